@@ -1,0 +1,164 @@
+"""Generate the golden fixtures under tests/golden/ from the REAL reference.
+
+Run in the build container only (it imports the read-only reference package
+from /root/reference/pkg/src). The GPU box never runs this script; it only
+reads the committed .npz files.
+
+    python tests/golden/make_golden.py
+
+Fixtures (all float64, reference arithmetic):
+  kernels_small.npz  block products / blocks / cross products, 3 families
+                     (mirrors tests/test_kernels.py:66-142, test_dist.py)
+  config1.npz        config 1 problem (n=2000 d=8 b=200 m=9 r=100 RBF):
+                     inputs, per-iteration records for t=0..4, the full
+                     500-iteration adasap_solve (block crc32s, stepsizes,
+                     final W), posterior mean and RMSE on the test points
+  config2.npz        one K[B,:]Z block product at config 2 / config 3 shape
+                     (n=1e5, b=1000, m=65; RBF d=11 and Matern-3/2 d=9);
+                     inputs are regenerated from seeds by the tests
+  randnla.npz        Nystrom factor, Woodbury applies, power stepsize
+  rng.npz            block crc32s / first draws for several (seed, t, n, b)
+"""
+
+import os
+import sys
+import zlib
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import sapgp  # noqa: E402  (the reference)
+from sapgp import dist as rdist  # noqa: E402
+from sapgp import randnla as rrand  # noqa: E402
+from sapgp import solvers as rsol  # noqa: E402
+from sapgp.rng import substream  # noqa: E402
+
+from paper_2505_13723_b200 import synthetic  # noqa: E402
+
+
+def kernels_small():
+    out = {}
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((60, 3))
+    M = rng.standard_normal((60, 4))
+    B = np.sort(rng.choice(60, 17, replace=False))
+    B = np.union1d(B, [0])  # the block contains index 0 (diagonal rule)
+    Xs = rng.standard_normal((7, 3))
+    omega = rng.standard_normal((B.size, 5))
+    X300 = rng.standard_normal((300, 3))
+    M300 = rng.standard_normal((300, 3))
+    out.update(X=X, M=M, B=B, Xs=Xs, omega=omega, X300=X300, M300=M300,
+               ls=np.array([0.9, 1.4, 0.6]), var=np.array(1.3))
+    for fam in ("rbf", "matern32", "matern52"):
+        spec = sapgp.KernelSpec(fam, np.array([0.9, 1.4, 0.6]), 1.3)
+        orc = sapgp.KernelOracle(spec, X, 0.1)
+        out[f"{fam}_KBM"] = rdist.col_dist_matmul(orc, M, B)
+        out[f"{fam}_KBB"] = orc.block(B)
+        out[f"{fam}_KBBom"] = rdist.row_dist_matmul(orc, omega, B)
+        out[f"{fam}_cross"] = orc.cross_matmul(Xs, M)
+        orc300 = sapgp.KernelOracle(spec, X300, 0.1)
+        out[f"{fam}_matmul300"] = orc300.matmul(M300)
+    np.savez_compressed(os.path.join(HERE, "kernels_small.npz"), **out)
+
+
+def config1():
+    n, d, b, m, r, lam, seed = 2000, 8, 200, 9, 100, 1e-2, 0
+    prob = synthetic.make_problem(n, d, "rbf", m, seed=seed, lam=lam)
+    spec = sapgp.KernelSpec("rbf", prob.lengthscales, prob.variance)
+    orc = sapgp.KernelOracle(spec, prob.X, lam)
+    cfg = sapgp.RunConfig(lam=lam, blocksize=b, nystrom_rank=r, residual_every=0,
+                          seed=seed)
+    accel = rsol.resolve_accel(cfg, n, b)
+    out = dict(X=prob.X, Y=prob.Y, Xtest=prob.Xtest, ytest=prob.ytest,
+               f_test=prob.f_test, ls=prob.lengthscales)
+    # per-iteration detail for the first iterations, through the reference's
+    # own step function (the Z passed to col_dist_matmul is the state's Z)
+    state = rsol.SolverState.zeros(n, m, accelerated=True)
+    for t in range(5):
+        Zt = state.Z.copy()
+        block = rsol._uniform_block(seed, t, n, b)
+        G = rdist.col_dist_matmul(orc, Zt, block)
+        omega = substream(seed, "omega", t).standard_normal((b, r))
+        sketch = rdist.row_dist_matmul(orc, omega, block)
+        fac = rrand.rand_nystrom_retry(sketch, omega, r)
+        state, eta, blk = rsol.adasap_step(orc, state, prob.Y, cfg, accel)
+        assert np.array_equal(blk, block)
+        out[f"t{t}_Z"] = Zt
+        out[f"t{t}_block"] = block
+        out[f"t{t}_G"] = G
+        out[f"t{t}_S"] = fac.S
+        out[f"t{t}_eta"] = np.array(eta)
+        out[f"t{t}_W"] = state.W.copy()
+    res = rsol.adasap_solve(orc, prob.Y, cfg)
+    out["final_W"] = res.W
+    out["iters"] = np.array(res.iterations)
+    out["crc"] = np.array([rec.block_hash for rec in res.trace.records], dtype=np.int64)
+    out["eta"] = np.array([rec.stepsize for rec in res.trace.records])
+    out["resid"] = np.array(res.trace.final_residual())
+    pm = orc.cross_matmul(prob.Xtest, res.W)
+    out["test_mean"] = pm
+    out["test_rmse"] = np.array(sapgp.rmse(pm[:, 0], prob.ytest))
+    np.savez_compressed(os.path.join(HERE, "config1.npz"), **out)
+
+
+def config2():
+    out = {}
+    for tag, fam, d in (("rbf_d11", "rbf", 11), ("m32_d9", "matern32", 9)):
+        n, b, m, seed = 100_000, 1000, 65, 0
+        X = synthetic.make_inputs(n, d, seed)
+        spec = sapgp.KernelSpec(fam, np.full(d, np.sqrt(d)), 1.0)
+        orc = sapgp.KernelOracle(spec, X, 1e-2)
+        Z = substream(seed, "golden_z").standard_normal((n, m))
+        B = rsol._uniform_block(seed, 0, n, b)
+        out[f"{tag}_B"] = B
+        out[f"{tag}_G"] = rdist.col_dist_matmul(orc, Z, B, sapgp.WorkerPool(8))
+    np.savez_compressed(os.path.join(HERE, "config2.npz"), **out)
+
+
+def randnla():
+    c1 = np.load(os.path.join(HERE, "config1.npz"))
+    X, ls = c1["X"], c1["ls"]
+    spec = sapgp.KernelSpec("rbf", ls, 1.0)
+    orc = sapgp.KernelOracle(spec, X, 1e-2)
+    B = c1["t1_block"]
+    Kbb = orc.block(B)
+    omega = substream(0, "omega", 1).standard_normal((B.size, 100))
+    sketch = Kbb @ omega
+    fac = rrand.rand_nystrom_retry(sketch, omega, 100)
+    rho = float(fac.S[-1]) + 1e-2
+    g = np.random.default_rng(3).standard_normal((B.size, 9))
+    eta = rrand.rand_power_stepsize(lambda v: Kbb @ v + 1e-2 * v, fac, rho, 10,
+                                    substream(0, "power", 1))
+    np.savez_compressed(
+        os.path.join(HERE, "randnla.npz"), Kbb=Kbb, omega=omega, S=fac.S,
+        P=fac.U @ fac.U.T, rho=np.array(rho), g=g,
+        inv=rrand.apply_inv(fac, rho, g), inv_sqrt=rrand.apply_inv_sqrt(fac, rho, g),
+        eta=np.array(eta))
+
+
+def rng_fixture():
+    rows = []
+    for seed, n, b in ((0, 2000, 200), (0, 100_000, 1000), (0, 1_000_000, 2000),
+                       (7, 10_000_000, 5000)):
+        for t in (0, 1, 2, 17, 499):
+            blk = rsol._uniform_block(seed, t, n, b)
+            rows.append((seed, n, b, t, zlib.crc32(blk.tobytes()), int(blk[0]), int(blk[-1])))
+    om = substream(0, "omega", 3).standard_normal((5, 4))
+    pw = substream(0, "power", 3).standard_normal(6)
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), rows=np.array(rows, dtype=np.int64),
+                        omega=om, power=pw)
+
+
+if __name__ == "__main__":
+    kernels_small()
+    config1()
+    config2()
+    randnla()
+    rng_fixture()
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
