@@ -1,0 +1,125 @@
+/*
+ * sapgp_b200.h -- C ABI of the B200-native ADASAP hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as void*; none allocates device memory (callers pass workspace)
+ * and none synchronises the stream. Return value: SAP_OK or an error code;
+ * sap_last_error() returns a thread-local message for the last failure.
+ *
+ * Status codes map onto the reference exception types (errors.py:4-29):
+ *   SAP_ERR_CONTRACT  -> ContractError   (shape/index/precondition)
+ *   SAP_ERR_NUMERICAL -> NumericalError
+ *   SAP_ERR_DEVICE    -> WorkerError     (CUDA launch/runtime failure)
+ *
+ * Reference interfaces replaced (paths relative to pkg/src/sapgp/):
+ *   sap_prepare_points  <- KernelOracle.__init__ / _scale      kernels.py:45-53, :100-112
+ *   sap_gather_points   <- self._scaled[rows], self._row_sq[rows] kernels.py:123-125
+ *   sap_krows_times     <- col_dist_matmul (ColDistMatMat)      dist.py:108-127
+ *                          row_dist_matmul (RowDistMatMat)      dist.py:130-147
+ *                          KernelOracle.tile + family values    kernels.py:56-66, :118-127
+ *                          KernelOracle.cross_matmul            kernels.py:161-176
+ *                          KernelOracle.matmul                  kernels.py:145-159
+ *   sap_ktile           <- KernelOracle.tile / .block / .dense   kernels.py:118-143
+ *   sap_grad_gather     <- grad = K[B,:]Z + lam Z[B] - Y[B]     solvers.py:376-377
+ *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
+ *   sap_combine         <- materialising W (or Z) from the lazy
+ *                          two-array Nesterov state
+ *
+ * Layouts (all row/column strides in elements):
+ *   point set   Xs[j*ldx + k] float32, scaled by 1/lengthscale, zero padded
+ *               to ldx (multiple of 4); sqn[j] = |Xs_j|^2 (computed in fp64)
+ *   RHS / state column-major n x m: element (row j, column c) at A[c*lda + j]
+ *   outputs     row-major b x m: out[i*ldo + c]
+ */
+#ifndef SAPGP_B200_H
+#define SAPGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAP_ABI_VERSION 1
+
+enum { SAP_OK = 0, SAP_ERR_CONTRACT = 1, SAP_ERR_NUMERICAL = 2, SAP_ERR_DEVICE = 3 };
+enum { SAP_RBF = 0, SAP_MATERN32 = 1, SAP_MATERN52 = 2 };
+
+int sap_abi_version(void);
+const char *sap_last_error(void);
+
+/* Number of kernels this library has launched in the process (diagnostics). */
+long long sap_launch_count(void);
+
+/* FP32 FFMA throughput probe: 148*4 CTAs x 256 threads x 8 chains x iters FFMA. */
+int sap_ffma_peak(float *out, int iters, void *stream);
+
+/* Xs = X / ls (fp64 math, fp32 store, zero padding up to ldx), sqn = |Xs|^2. */
+int sap_prepare_points(const double *X, int64_t n, int d, const double *inv_ls,
+                       float *Xs, int ldx, float *sqn, void *stream);
+
+/* Rs[i] = Xs[idx[i] - base], rsqn[i] = sqn[idx[i] - base]. */
+int sap_gather_points(const float *Xs, const float *sqn, int ldx, const int64_t *idx,
+                      int64_t b, int64_t base, float *Rs, float *rsqn, void *stream);
+
+/* Workspace bytes sap_krows_times needs for (b rows, m columns, ncols points). */
+size_t sap_krows_workspace(int64_t b, int m, int64_t ncols);
+
+/*
+ * out[i, c] (=, or += if accumulate) variance * sum_j k(r_i, x_j) * R[j, c]
+ * with R = ca*A + cb*Bm (Bm may be NULL), k the family's unit-variance kernel
+ * on scaled points, distances in expansion form clamped at 0 (kernels.py:125).
+ * Diagonal rule (kernels.py:126): when row_ids != NULL, entries whose global
+ * row id equals the global column id (col_ids[j] if col_ids != NULL else
+ * col_base + j) use squared distance exactly 0. Reduction order over the
+ * column dimension is fixed for given (b, m, ncols): results are
+ * run-to-run deterministic.
+ */
+int sap_krows_times(const float *Xs, const float *sqn, int ldx, int64_t ncols,
+                    const int64_t *col_ids, int64_t col_base,
+                    const float *Rs, const float *rsqn, const int64_t *row_ids, int64_t b,
+                    int d, const float *A, const float *Bm, int64_t lda, int m,
+                    double ca, double cb, int family, double variance,
+                    float *out, int64_t ldo, int accumulate,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Dense tile out[i, j] = variance * k(a_i, c_j) (fp64 out, kernels.py:118-127).
+ * When row_ids and col_ids are both non-NULL, entries with equal ids are
+ * exactly `variance` (kernels.py:126, :135). With a == c and equal id arrays
+ * the result is bitwise symmetric: K[B,B] of kernels.py:129-136.
+ */
+int sap_ktile(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+              const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc,
+              int ldx, int d, int family, double variance, double *out, int64_t ldo,
+              void *stream);
+
+/*
+ * g[i, c] = G[i, c] + (own(i) ? lam * Z[j, c] - Y[j, c] : 0), j = loc[i],
+ * Z = zp*P + zq*Q; rows with loc[i] < 0 belong to another shard.
+ */
+int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q,
+                    const float *Y, int64_t ldp, double zp, double zq,
+                    const int64_t *loc, int64_t b, int m, double lam,
+                    double *g, int64_t ldgo, void *stream);
+
+/*
+ * Block-row Nesterov step in the lazy basis: for owned rows
+ *   WB[i, c] = Z[j, c] - eta * D[i, c]          (Z = zp*P + zq*Q, old basis)
+ *   P[j, c] += e0 * eta * D[i, c];  Q[j, c] += e1 * eta * D[i, c]
+ * eta is read from device memory (eta_dev[0]).
+ */
+int sap_pq_update(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b, int m,
+                  const double *D, int64_t ldd, const double *eta_dev,
+                  double zp, double zq, double e0, double e1,
+                  float *WB, int64_t ldwb, void *stream);
+
+/* out = a*P + b*Q (column-major n x m, ld ldp); Q may be NULL (b ignored). */
+int sap_combine(float *out, int64_t ldo, const float *P, const float *Q, int64_t ldp,
+                int64_t n, int m, double a, double b, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAPGP_B200_H */

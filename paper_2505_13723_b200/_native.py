@@ -1,0 +1,99 @@
+"""ctypes binding of libsapgp_b200.so (the C ABI in include/sapgp_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2505_13723_b200/csrc``). There is no fallback: if the
+library is missing, or no CUDA device is visible when a device entry point
+is called, this module raises ``WorkerError`` -- the package never computes
+the hot path on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from .errors import ContractError, NumericalError, WorkerError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsapgp_b200.so")
+
+SAP_OK, SAP_ERR_CONTRACT, SAP_ERR_NUMERICAL, SAP_ERR_DEVICE = 0, 1, 2, 3
+FAMILY_CODES = {"rbf": 0, "matern32": 1, "matern52": 2}
+ABI_VERSION = 1
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); mirrors include/sapgp_b200.h exactly
+SIGNATURES = {
+    "sap_abi_version": (_I, []),
+    "sap_last_error": (ctypes.c_char_p, []),
+    "sap_launch_count": (ctypes.c_longlong, []),
+    "sap_ffma_peak": (_I, [_P, _I, _P]),
+    "sap_prepare_points": (_I, [_P, _I64, _I, _P, _P, _I, _P, _P]),
+    "sap_gather_points": (_I, [_P, _P, _I, _P, _I64, _I64, _P, _P, _P]),
+    "sap_krows_workspace": (_SZ, [_I64, _I, _I64]),
+    "sap_krows_times": (_I, [_P, _P, _I, _I64, _P, _I64, _P, _P, _P, _I64, _I, _P, _P, _I64, _I,
+                             _D, _D, _I, _D, _P, _I64, _I, _P, _SZ, _P]),
+    "sap_ktile": (_I, [_P, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _I, _D, _P, _I64, _P]),
+    "sap_grad_gather": (_I, [_P, _I64, _P, _P, _P, _I64, _D, _D, _P, _I64, _I, _D, _P, _I64, _P]),
+    "sap_pq_update": (_I, [_P, _P, _I64, _P, _I64, _I, _P, _I64, _P, _D, _D, _D, _D, _P, _I64,
+                           _P]),
+    "sap_combine": (_I, [_P, _I64, _P, _P, _I64, _I64, _I, _D, _D, _P]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the shared library; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise WorkerError(
+            f"CUDA library {LIB_PATH} is not built; run __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.sap_abi_version() != ABI_VERSION:
+        raise WorkerError("libsapgp_b200.so ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise WorkerError("no CUDA device visible: the B200 path has no CPU fallback")
+
+
+def check(rc):
+    if rc == SAP_OK:
+        return
+    msg = load().sap_last_error().decode("utf-8", "replace")
+    if rc == SAP_ERR_CONTRACT:
+        raise ContractError(msg)
+    if rc == SAP_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    raise WorkerError(msg)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def call(name, *args):
+    check(getattr(load(), name)(*args))

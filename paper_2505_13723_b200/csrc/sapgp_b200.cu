@@ -1,0 +1,367 @@
+// C-ABI entry points of libsapgp_b200.so (declared in include/sapgp_b200.h)
+// plus the small HBM-bound kernels around the block-row product.
+#include <cstdio>
+#include <cstdarg>
+#include <string>
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+#include "krows_ffma.cuh"
+
+namespace sap {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+std::atomic<long long> g_launches{0};
+
+int check_launch(const char *what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SAP_ERR_DEVICE, "%s: %s", what, cudaGetErrorString(e));
+  return SAP_OK;
+}
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// point preparation / gathers
+
+__global__ void prepare_points_kernel(const double *X, int64_t n, int d, const double *inv_ls,
+                                      float *Xs, int ldx, float *sqn) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < ldx; ++k) {
+    double v = 0.0;
+    if (k < d) {
+      v = X[j * d + k] * inv_ls[k];
+      s = fma(v, v, s);
+    }
+    Xs[j * ldx + k] = float(v);
+  }
+  sqn[j] = float(s);
+}
+
+__global__ void gather_points_kernel(const float *Xs, const float *sqn, int ldx,
+                                     const int64_t *idx, int64_t b, int64_t base, float *Rs,
+                                     float *rsqn) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * ldx) return;
+  const int64_t i = e / ldx;
+  const int k = int(e % ldx);
+  const int64_t j = idx[i] - base;
+  Rs[e] = Xs[j * ldx + k];
+  if (k == 0) rsqn[i] = sqn[j];
+}
+
+// ---------------------------------------------------------------------------
+// dense tiles (kernels.py:118-143). With equal point sets and id arrays the
+// result is bitwise symmetric: (rn_i + rn_j) - 2 sum_k a_k c_k is symmetric
+// term by term in IEEE arithmetic.
+
+template <int FAM>
+__global__ void ktile_kernel(const float *Ra, const float *rasqn, const int64_t *row_ids,
+                             int64_t na, const float *Rc, const float *rcsqn,
+                             const int64_t *col_ids, int64_t nc, int ldx, int d, float variance,
+                             double *out, int64_t ldo) {
+  const int64_t i = int64_t(blockIdx.y) * blockDim.y + threadIdx.y;
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= na || j >= nc) return;
+  float v;
+  if (row_ids && col_ids && row_ids[i] == col_ids[j]) {
+    v = variance;
+  } else {
+    float dot = 0.0f;
+    for (int k = 0; k < d; ++k) dot = fmaf(Ra[i * ldx + k], Rc[j * ldx + k], dot);
+    const float sq = fmaf(-2.0f, dot, rasqn[i] + rcsqn[j]);
+    v = variance * kernel_value<FAM>(sq);
+  }
+  out[i * ldo + j] = double(v);
+}
+
+// ---------------------------------------------------------------------------
+// gradient gather (solvers.py:376-377), lazy Nesterov rows, materialisation
+
+__global__ void grad_gather_kernel(const float *G, int64_t ldg, const float *P, const float *Q,
+                                   const float *Y, int64_t ldp, double zp, double zq,
+                                   const int64_t *loc, int64_t b, int m, double lam, double *g,
+                                   int64_t ldgo) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * m) return;
+  const int64_t i = e / m;
+  const int c = int(e % m);
+  double v = double(G[i * ldg + c]);
+  const int64_t j = loc[i];
+  if (j >= 0) {
+    const int64_t o = int64_t(c) * ldp + j;
+    double z = zp * double(P[o]);
+    if (Q) z += zq * double(Q[o]);
+    v += lam * z - double(Y[o]);
+  }
+  g[i * ldgo + c] = v;
+}
+
+__global__ void pq_update_kernel(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b,
+                                 int m, const double *D, int64_t ldd, const double *eta_dev,
+                                 double zp, double zq, double e0, double e1, float *WB,
+                                 int64_t ldwb) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * m) return;
+  const int64_t i = e / m;
+  const int c = int(e % m);
+  const int64_t j = loc[i];
+  if (j < 0) return;
+  const double eta = eta_dev[0];
+  const double dd = D[i * ldd + c];
+  const int64_t o = int64_t(c) * ldp + j;
+  const double p = P[o];
+  const double q = Q ? double(Q[o]) : 0.0;
+  if (WB) WB[i * ldwb + c] = float(zp * p + zq * q - eta * dd);
+  P[o] = float(p + e0 * eta * dd);
+  if (Q) Q[o] = float(q + e1 * eta * dd);
+}
+
+__global__ void combine_kernel(float *out, int64_t ldo, const float *P, const float *Q,
+                               int64_t ldp, int64_t n, int m, float a, float bq) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * m) return;
+  const int c = int(e / n);
+  const int64_t j = e % n;
+  float v = a * P[int64_t(c) * ldp + j];
+  if (Q) v = fmaf(bq, Q[int64_t(c) * ldp + j], v);
+  out[int64_t(c) * ldo + j] = v;
+}
+
+// Fixed-order reduction of the split partials: out = variance * sum_s part[s].
+__global__ void krows_reduce_kernel(const float *__restrict__ part, int splits, int64_t b, int m,
+                                    float variance, float *out, int64_t ldo, int c0,
+                                    int accumulate) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * m) return;
+  const int64_t i = e / m;
+  const int c = int(e % m);
+  float s = 0.0f;
+  for (int k = 0; k < splits; ++k) s += part[int64_t(k) * b * m + e];
+  float *o = out + i * ldo + c0 + c;
+  const float v = variance * s;
+  *o = accumulate ? *o + v : v;
+}
+
+
+// ---------------------------------------------------------------------------
+// FP32 FFMA throughput probe (the roofline denominator of the FFMA path):
+// 8 independent dependency chains per thread, 2 flops per FFMA.
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3f + k;
+  const float x = 0.9999f, y = 1e-4f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], x, y);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+// ---------------------------------------------------------------------------
+// krows dispatch
+
+constexpr int kTargetCtas = 2 * 148;  // a pure function of the shape: deterministic
+
+int pick_splits(int64_t b, int m, int64_t tiles) {
+  const int64_t row_tiles = (b + kFfmaBM - 1) / kFfmaBM;
+  const int64_t m_chunks = (m + 127) / 128;
+  int64_t s = (kTargetCtas + row_tiles * m_chunks - 1) / (row_tiles * m_chunks);
+  s = std::min<int64_t>(s, std::max<int64_t>(1, tiles / 8));
+  return int(std::max<int64_t>(1, std::min<int64_t>(s, 1024)));
+}
+
+int launch_ffma_rbf(KrowsParams p, int dp, cudaStream_t st);
+int launch_ffma_m32(KrowsParams p, int dp, cudaStream_t st);
+int launch_ffma_m52(KrowsParams p, int dp, cudaStream_t st);
+
+int padded_dim(int ldx) {
+  for (int dp : {4, 8, 12, 16, 32, 64})
+    if (ldx <= dp) return dp;
+  return -1;
+}
+
+}  // namespace sap
+
+using namespace sap;
+
+extern "C" {
+
+int sap_abi_version(void) { return SAP_ABI_VERSION; }
+
+const char *sap_last_error(void) { return g_last_error.c_str(); }
+
+long long sap_launch_count(void) { return g_launches.load(); }
+
+int sap_ffma_peak(float *out, int iters, void *stream) {
+  ffma_peak_kernel<<<148 * 4, 256, 0, S(stream)>>>(out, iters);
+  return check_launch("ffma_peak_kernel");
+}
+
+int sap_prepare_points(const double *X, int64_t n, int d, const double *inv_ls, float *Xs, int ldx,
+                       float *sqn, void *stream) {
+  if (n < 0 || d < 1 || ldx < d || ldx % 4 != 0)
+    return fail(SAP_ERR_CONTRACT, "prepare_points: bad shape n=%lld d=%d ldx=%d",
+                (long long)n, d, ldx);
+  if (n == 0) return SAP_OK;
+  prepare_points_kernel<<<unsigned((n + 255) / 256), 256, 0, S(stream)>>>(X, n, d, inv_ls, Xs, ldx,
+                                                                         sqn);
+  return check_launch("prepare_points_kernel");
+}
+
+int sap_gather_points(const float *Xs, const float *sqn, int ldx, const int64_t *idx, int64_t b,
+                      int64_t base, float *Rs, float *rsqn, void *stream) {
+  if (b <= 0) return fail(SAP_ERR_CONTRACT, "gather_points: empty index block");
+  const int64_t tot = b * ldx;
+  gather_points_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(Xs, sqn, ldx, idx, b,
+                                                                          base, Rs, rsqn);
+  return check_launch("gather_points_kernel");
+}
+
+size_t sap_krows_workspace(int64_t b, int m, int64_t ncols) {
+  const int64_t tiles = (ncols + kFfmaBN - 1) / kFfmaBN;
+  const int mc = m < 128 ? m : 128;
+  const int s = pick_splits(b, mc, tiles);
+  return s > 1 ? size_t(s) * size_t(b) * size_t(mc) * sizeof(float) : 0;
+}
+
+int sap_krows_times(const float *Xs, const float *sqn, int ldx, int64_t ncols,
+                    const int64_t *col_ids, int64_t col_base, const float *Rs, const float *rsqn,
+                    const int64_t *row_ids, int64_t b, int d, const float *A, const float *Bm,
+                    int64_t lda, int m, double ca, double cb, int family, double variance,
+                    float *out, int64_t ldo, int accumulate, void *ws, size_t ws_bytes,
+                    void *stream) {
+  if (b <= 0 || m <= 0 || ncols < 0 || d < 1)
+    return fail(SAP_ERR_CONTRACT, "krows_times: bad shape b=%lld m=%d ncols=%lld d=%d",
+                (long long)b, m, (long long)ncols, d);
+  if (ldx < d || ldx % 4 != 0) return fail(SAP_ERR_CONTRACT, "krows_times: ldx=%d", ldx);
+  if (lda < ncols) return fail(SAP_ERR_CONTRACT, "krows_times: lda < ncols");
+  if (ldo < m) return fail(SAP_ERR_CONTRACT, "krows_times: ldo < m");
+  if (family < SAP_RBF || family > SAP_MATERN52)
+    return fail(SAP_ERR_CONTRACT, "krows_times: unknown family %d", family);
+  const int dp = padded_dim(ldx);
+  if (dp < 0) return fail(SAP_ERR_CONTRACT, "krows_times: d=%d exceeds 64", d);
+  if (ldx != dp)
+    return fail(SAP_ERR_CONTRACT, "krows_times: ldx=%d must equal the padded width %d", ldx, dp);
+  cudaStream_t st = S(stream);
+  if (ncols == 0) {
+    if (!accumulate) {
+      for (int64_t i = 0; i < b; ++i)
+        if (cudaMemsetAsync(out + i * ldo, 0, sizeof(float) * m, st) != cudaSuccess)
+          return fail(SAP_ERR_DEVICE, "memset failed");
+    }
+    return SAP_OK;
+  }
+  KrowsParams p{};
+  p.Xs = Xs; p.sqn = sqn; p.ldx = ldx; p.ncols = ncols; p.col_ids = col_ids;
+  p.col_base = col_base; p.Rs = Rs; p.rsqn = rsqn; p.row_ids = row_ids; p.b = b;
+  p.A = A; p.Bm = Bm; p.lda = lda; p.ca = float(ca); p.cb = float(cb);
+  p.variance = float(variance); p.ldo = ldo; p.accumulate = accumulate;
+  p.tiles = (ncols + kFfmaBN - 1) / kFfmaBN;
+  for (int c0 = 0; c0 < m; c0 += 128) {
+    const int mc = std::min(128, m - c0);
+    p.m = mc;
+    p.c0 = c0;
+    p.splits = pick_splits(b, mc, p.tiles);
+    if (p.splits > 1) {
+      const size_t need = size_t(p.splits) * size_t(b) * size_t(mc) * sizeof(float);
+      if (!ws || ws_bytes < need)
+        return fail(SAP_ERR_CONTRACT, "krows_times: workspace %zu < %zu bytes", ws_bytes, need);
+      p.out = static_cast<float *>(ws);
+    } else {
+      p.out = out;
+    }
+    int rc;
+    switch (family) {
+      case SAP_RBF: rc = launch_ffma_rbf(p, dp, st); break;
+      case SAP_MATERN32: rc = launch_ffma_m32(p, dp, st); break;
+      default: rc = launch_ffma_m52(p, dp, st); break;
+    }
+    if (rc != SAP_OK) return rc;
+    if (p.splits > 1) {
+      const int64_t tot = b * mc;
+      krows_reduce_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(
+          static_cast<const float *>(ws), p.splits, b, mc, float(variance), out, ldo, c0,
+          accumulate);
+      if ((rc = check_launch("krows_reduce_kernel")) != SAP_OK) return rc;
+    }
+  }
+  return SAP_OK;
+}
+
+int sap_ktile(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+              const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc, int ldx,
+              int d, int family, double variance, double *out, int64_t ldo, void *stream) {
+  if (na <= 0 || nc <= 0 || ldo < nc || ldx < d || d < 1)
+    return fail(SAP_ERR_CONTRACT, "ktile: bad shape");
+  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 7) / 8));
+  cudaStream_t st = S(stream);
+  const float var = float(variance);
+  switch (family) {
+    case SAP_RBF:
+      ktile_kernel<SAP_RBF><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids, nc,
+                                                  ldx, d, var, out, ldo);
+      break;
+    case SAP_MATERN32:
+      ktile_kernel<SAP_MATERN32><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
+                                                       nc, ldx, d, var, out, ldo);
+      break;
+    case SAP_MATERN52:
+      ktile_kernel<SAP_MATERN52><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
+                                                       nc, ldx, d, var, out, ldo);
+      break;
+    default: return fail(SAP_ERR_CONTRACT, "ktile: unknown family %d", family);
+  }
+  return check_launch("ktile_kernel");
+}
+
+int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q, const float *Y,
+                    int64_t ldp, double zp, double zq, const int64_t *loc, int64_t b, int m,
+                    double lam, double *g, int64_t ldgo, void *stream) {
+  if (b <= 0 || m <= 0) return fail(SAP_ERR_CONTRACT, "grad_gather: bad shape");
+  const int64_t tot = b * m;
+  grad_gather_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
+      G, ldg, P, Q, Y, ldp, zp, zq, loc, b, m, lam, g, ldgo);
+  return check_launch("grad_gather_kernel");
+}
+
+int sap_pq_update(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b, int m,
+                  const double *D, int64_t ldd, const double *eta_dev, double zp, double zq,
+                  double e0, double e1, float *WB, int64_t ldwb, void *stream) {
+  if (b <= 0 || m <= 0) return fail(SAP_ERR_CONTRACT, "pq_update: bad shape");
+  const int64_t tot = b * m;
+  pq_update_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
+      P, Q, ldp, loc, b, m, D, ldd, eta_dev, zp, zq, e0, e1, WB, ldwb);
+  return check_launch("pq_update_kernel");
+}
+
+int sap_combine(float *out, int64_t ldo, const float *P, const float *Q, int64_t ldp, int64_t n,
+                int m, double a, double b, void *stream) {
+  if (n < 0 || m <= 0) return fail(SAP_ERR_CONTRACT, "combine: bad shape");
+  if (n == 0) return SAP_OK;
+  const int64_t tot = n * m;
+  combine_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(out, ldo, P, Q, ldp, n, m,
+                                                                    float(a), float(b));
+  return check_launch("combine_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+"""Lookahead producer of the iterate-independent ADASAP phases.
+
+In one ADASAP iteration t (solvers.py:361-403) everything except the
+block-row product and the update depends only on (seed, t) and X:
+
+    B_t      = sort(substream(seed, "block", t).choice(n, b))    solvers.py:375
+    Omega_t  = substream(seed, "omega", t).standard_normal((b, r)) :384
+    sketch   = K[B,B] Omega_t                                     :385
+    (U, S)   = rand_nystrom_retry(sketch, Omega_t, r)             :386
+    rho      = S[-1] + lam                                         :387
+    eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
+                                   10, substream(seed, "power", t)) :389-396
+
+so they are produced ``L = config.lookahead`` iterations at a time, on a
+side CUDA stream and a host worker thread, while the main stream runs the
+previous batch's block-row products. Per batch there is one device->host
+round trip (three r x r matrices per iteration) for the host LAPACK part
+(``randnla.factor_core_retry``); everything dimension-b runs on the GPU in
+fp64 (QR of the sketch, U = Qs Ur, the batched power iteration). Buffers
+live in two preallocated slots reused under CUDA events, so nothing is
+allocated in steady state.
+"""
+
+from __future__ import annotations
+
+import math
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .errors import NumericalError
+from .randnla import factor_core_retry
+from .rng import block_hash, substream, uniform_block
+
+
+@dataclass
+class IterPlan:
+    t: int
+    block: np.ndarray          # host, sorted int64
+    crc: int
+    block_dev: torch.Tensor    # (b,) int64 global ids
+    loc_dev: torch.Tensor      # (b,) int64 local row or -1
+    Xb: torch.Tensor           # (b, ldx) fp32 gathered points
+    rsq: torch.Tensor          # (b,) fp32
+    U: torch.Tensor | None     # (b, r) fp64
+    Mc: torch.Tensor | None    # (r,) fp64, Woodbury core diag S/(S+rho) (0 on pruned modes)
+    rho: float
+    eta_dev: torch.Tensor      # (1,) fp64 view
+    S: np.ndarray
+
+
+class _Slot:
+    def __init__(self, L, b, r, ldx, dev):
+        f32, f64, i64 = torch.float32, torch.float64, torch.int64
+        self.block_dev = torch.empty((L, b), dtype=i64, device=dev)
+        self.loc_dev = torch.empty((L, b), dtype=i64, device=dev)
+        self.Xb = torch.empty((L, b, ldx), dtype=f32, device=dev)
+        self.rsq = torch.empty((L, b), dtype=f32, device=dev)
+        self.U = torch.empty((L, b, r), dtype=f64, device=dev) if r else None
+        self.Mc = torch.empty((L, r), dtype=f64, device=dev) if r else None
+        self.eta = torch.empty(L, dtype=f64, device=dev)
+        self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
+        pin = torch.cuda.is_available()
+        self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
+        self.h_omega = torch.empty((L, b, max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_v0 = torch.empty((L, b), dtype=f64, pin_memory=pin)
+        self.h_small = torch.empty((L, 3, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_ur = torch.empty((L, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_coef = torch.empty((L, 3, max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_rho = torch.empty(L, dtype=f64, pin_memory=pin)
+        self.free = None      # event on the main stream: last consumer enqueued
+        self.h2d_done = None  # event on the side stream: pinned inputs consumed
+
+
+@dataclass
+class _Batch:
+    slot: _Slot
+    t0: int
+    count: int
+    blocks: list
+    crcs: list
+    rho: np.ndarray
+    S: list
+    ready: torch.cuda.Event = field(default=None)
+
+
+class Lookahead:
+    """Produces IterPlan(t) for t = 0..total-1 in batches of ``L``."""
+
+    def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10):
+        self.o, self.shard, self.seed = oracle, shard, seed
+        self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
+        self.total, self.L = total, max(1, min(L, total))
+        self.iters = power_iters
+        dev = oracle.device
+        self.dev = dev
+        self.side = torch.cuda.Stream(device=dev)
+        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev) for _ in range(2)]
+        self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sap-lookahead")
+        self.cur = None
+        self.k = 0
+        self.fut = self.pool.submit(self._produce, self.slots[0], 0, min(self.L, total))
+
+    def close(self):
+        self.pool.shutdown(wait=True)
+
+    # -- consumer side (main thread) ------------------------------------------
+    def get(self, t):
+        cur = self.cur
+        if cur is None or t >= cur.t0 + cur.count:
+            main = torch.cuda.current_stream(self.dev)
+            if cur is not None:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                cur.slot.free = ev
+            cur = self.fut.result()
+            main.wait_event(cur.ready)
+            self.cur = cur
+            self.k += 1
+            nxt = cur.t0 + cur.count
+            if nxt < self.total:
+                self.fut = self.pool.submit(self._produce, self.slots[self.k % 2], nxt,
+                                            min(self.L, self.total - nxt))
+        i = t - cur.t0
+        s = cur.slot
+        return IterPlan(
+            t=t, block=cur.blocks[i], crc=cur.crcs[i], block_dev=s.block_dev[i],
+            loc_dev=s.loc_dev[i], Xb=s.Xb[i], rsq=s.rsq[i],
+            U=None if s.U is None else s.U[i], Mc=None if s.Mc is None else s.Mc[i],
+            rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i])
+
+    def check_flags(self):
+        """Raise if any power iteration failed (checked once, at the end)."""
+        for s in self.slots:
+            if int(s.bad.max()) != 0:
+                raise NumericalError("power iteration failed (collapsed or nonpositive Rayleigh "
+                                     "estimate; H is not PSD)")
+
+    # -- producer side (worker thread) ------------------------------------------
+    def _produce(self, slot, t0, count):
+        b, r, seed, n = self.b, self.r, self.seed, self.n
+        if slot.h2d_done is not None:
+            slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
+        blocks, crcs = [], []
+        for i in range(count):
+            t = t0 + i
+            blk = uniform_block(seed, t, n, b).astype(np.int64)
+            blocks.append(blk)
+            crcs.append(block_hash(blk))
+            slot.h_block[i].numpy()[:] = blk
+            if r:
+                slot.h_omega[i].numpy()[:] = substream(seed, "omega", t).standard_normal((b, r))
+            rng = substream(seed, "power", t)
+            v = rng.standard_normal(b)
+            nv = np.linalg.norm(v)
+            if nv == 0.0:
+                v = rng.standard_normal(b)
+                nv = np.linalg.norm(v)
+                if nv == 0.0:
+                    raise NumericalError("power iteration start vector is zero")
+            slot.h_v0[i].numpy()[:] = v / nv
+        side = self.side
+        pts = self.o.points
+        with torch.cuda.device(self.dev), torch.cuda.stream(side):
+            if slot.free is not None:
+                side.wait_event(slot.free)
+            slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
+            v0 = slot.h_v0[:count].to(self.dev, non_blocking=True)
+            om = slot.h_omega[:count].to(self.dev, non_blocking=True) if r else None
+            slot.h2d_done = torch.cuda.Event()
+            slot.h2d_done.record(side)
+            bd = slot.block_dev[:count]
+            slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
+            Kbb = torch.empty((count, b, b), dtype=torch.float64, device=self.dev)
+            sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
+            for i in range(count):
+                Xb, rsq = pts.gather(bd[i], out=(slot.Xb[i], slot.rsq[i]))
+                Kbb[i] = K.ktile(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d)
+                if r:
+                    omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS
+                    K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
+                                  sketch[i], col_ids=bd[i])
+            if r:
+                Y = sketch.to(torch.float64)
+                Q, R = torch.linalg.qr(Y)
+                small = torch.stack([R, om.transpose(1, 2) @ Y, om.transpose(1, 2) @ om], dim=1)
+                slot.h_small[:count].copy_(small, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+        rho = np.empty(count)
+        Ss = []
+        if r:
+            ev.synchronize()
+            hs = slot.h_small[:count].numpy()
+            hom = slot.h_omega
+            for i in range(count):
+                Ur, S, _ = factor_core_retry(hs[i, 0], hs[i, 1], hs[i, 2], r,
+                                             omega_rank=lambda i=i: np.linalg.matrix_rank(
+                                                 hom[i].numpy()))
+                rho[i] = float(S[-1]) + self.lam
+                keep = S > 0.0
+                slot.h_ur[i].numpy()[:] = Ur
+                slot.h_coef[i, 0].numpy()[:] = np.where(keep, S / (S + rho[i]), 0.0)
+                slot.h_coef[i, 1].numpy()[:] = 1.0 / np.sqrt(S + rho[i]) - 1.0 / math.sqrt(rho[i])
+                Ss.append(S)
+        else:
+            rho[:] = 1.0
+            Ss = [np.zeros(0)] * count
+        slot.h_rho[:count].numpy()[:] = rho
+        with torch.cuda.device(self.dev), torch.cuda.stream(side):
+            rho_d = slot.h_rho[:count].to(self.dev, non_blocking=True)
+            if r:
+                Ur = slot.h_ur[:count].to(self.dev, non_blocking=True)
+                coef = slot.h_coef[:count].to(self.dev, non_blocking=True)
+                torch.bmm(Q, Ur, out=slot.U[:count])
+                slot.Mc[:count].copy_(coef[:, 0])
+                E = coef[:, 1]
+                U = slot.U[:count]
+            self._power(Kbb, v0, rho_d, U if r else None, E if r else None, slot, count)
+            ready = torch.cuda.Event()
+            ready.record(side)
+            done = torch.cuda.Event()
+            done.record(side)
+            slot.h2d_done = done  # pinned host buffers reusable after this point
+        return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready)
+
+    def _power(self, Kbb, v, rho, U, E, slot, count):
+        """Batched rand_power_stepsize (randnla.py:165-196) on P^{-1/2}(K+lam)P^{-1/2},
+        P^{-1/2} x = x/sqrt(rho) + U diag((S+rho)^{-1/2} - rho^{-1/2}) U^T x."""
+        isr = rho.rsqrt()[:, None]
+
+        def pinv_sqrt(x):
+            y = x * isr
+            if U is not None:
+                y = y + torch.bmm(U, (E * torch.bmm(U.transpose(1, 2), x[:, :, None])[:, :, 0])
+                                  [:, :, None])[:, :, 0]
+            return y
+
+        bad = torch.zeros(count, dtype=torch.bool, device=self.dev)
+        est = None
+        for _ in range(self.iters):
+            w = pinv_sqrt(v)
+            z = torch.bmm(Kbb, w[:, :, None])[:, :, 0] + self.lam * w
+            y = pinv_sqrt(z)
+            est = (v * y).sum(dim=1)
+            ny = torch.linalg.vector_norm(y, dim=1)
+            bad |= ny == 0
+            v = y / ny[:, None]
+        bad |= est <= 0
+        slot.eta[:count].copy_(1.0 / est)
+        slot.bad[:count].bitwise_or_(bad.to(torch.int32))
+
+
+class _Cols:
+    """A gathered point subset viewed as a column point set."""
+
+    def __init__(self, pts, Xs, sqn):
+        self.Xs, self.sqn = Xs, sqn
+        self.n, self.d, self.ldx, self.device = Xs.shape[0], pts.d, pts.ldx, pts.device

@@ -1,0 +1,548 @@
+"""ADASAP on B200: drop-in mirror of ``sapgp.solvers`` (solvers.py:1-615).
+
+Same public names and semantics (``AccelParams``, ``resolve_accel``,
+``nesterov_update``, ``ConvergenceTrace``, ``SolverState``, ``SolveResult``,
+``adasap_step``, ``adasap_solve``, ``solve``), with the iteration executed
+by ``AdasapEngine``:
+
+* Phase I  -- K[B,:] Z by ``sap_krows_times`` over this rank's shard, then
+  the gradient gather g = K[B,:]Z + lam Z[B] - Y[B] (``sap_grad_gather``) and,
+  with several GPUs, one float64 all-reduce of g (paper Alg. 6);
+* Phases II/III -- produced ahead, batched, by ``pipeline.Lookahead``;
+* Phase IV -- D_B = (g - U diag(S/(S+rho)) U^T g) / rho (two fp64 GEMMs,
+  randnla.py:109-134 with U^T U = I) and the Nesterov update.
+
+The Nesterov update never touches the n - b rows outside the block. Off
+the block the recurrence (solvers.py:76-85) is the fixed linear map
+T = [[beta, 1-beta], [alpha, 1-alpha]] on the row pair (V, Z), so the
+engine stores two arrays (P, Q) and a 2 x 2 basis M with
+[V; Z] = M [P; Q] row-wise: untouched rows follow M <- T M for free, and
+the b block rows get an axpy (``sap_pq_update``). M starts at T's
+eigenbasis, which keeps it well conditioned; one column decays like
+(beta - alpha)^t and is renormalised by a rare dense rescale. W is
+materialised only when asked for (end of solve, residuals, tail averaging,
+callbacks). DESIGN.md §4 has the derivation.
+
+Deviations (documented, none changes the iterates beyond fp32 rounding):
+arithmetic on the state and the block product is fp32 (reference fp64);
+the per-iteration trace ``seconds`` is host enqueue time unless a residual
+is due; errors inside the lookahead surface at the start of the batch that
+contains the failing iteration.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .dist import WorkerPool
+from .errors import ConfigError, ContractError
+from .kernels import KernelOracle, krows_times, to_colmajor
+from .parallel import ShardInfo, allreduce_sum_, current_shard
+from .pipeline import Lookahead
+from .rng import block_hash
+
+DIVERGENCE_FACTOR = 1e6
+SDD_MOMENTUM = 0.9
+RENORM_LO, RENORM_HI = 2.0 ** -20, 2.0 ** 20
+
+
+# ---------------------------------------------------------------------------
+# acceleration parameters and the Nesterov recurrence (solvers.py:32-85)
+
+
+@dataclass(frozen=True)
+class AccelParams:
+    mu: float
+    nu: float
+
+    def __post_init__(self):
+        if not (self.mu > 0.0 and self.nu > 0.0):
+            raise ContractError("acceleration parameters must be positive")
+
+    @property
+    def beta(self):
+        return 1.0 - math.sqrt(self.mu / self.nu)
+
+    @property
+    def gamma(self):
+        return 1.0 / math.sqrt(self.mu * self.nu)
+
+    @property
+    def alpha(self):
+        return 1.0 / (1.0 + self.gamma * self.nu)
+
+
+@dataclass(frozen=True)
+class RawAccel:
+    beta: float
+    gamma: float
+    alpha: float
+
+
+NO_ACCELERATION = RawAccel(beta=1.0, gamma=0.0, alpha=0.0)
+
+
+def resolve_accel(config, n, blocksize):
+    """mu = lam, nu = n / blocksize by default (solvers.py:69-73)."""
+    mu = config.lam if config.mu == "default" else float(config.mu)
+    nu = n / blocksize if config.nu == "default" else float(config.nu)
+    return AccelParams(mu, nu)
+
+
+def nesterov_update(W, V, Z, direction, eta, beta, gamma, alpha):
+    """W' = Z - eta D; V' = beta V + (1-beta) Z - gamma eta D; Z' = alpha V + (1-alpha) W'
+    (solvers.py:76-85). Elementwise; runs on whatever device the inputs live on."""
+    W_next = Z - eta * direction
+    V_next = beta * V + (1.0 - beta) * Z - (gamma * eta) * direction
+    Z_next = alpha * V + (1.0 - alpha) * W_next
+    return W_next, V_next, Z_next
+
+
+# ---------------------------------------------------------------------------
+# traces, averaging, results (solvers.py:92-211)
+
+
+@dataclass
+class TraceRecord:
+    iteration: int
+    seconds: float
+    passes: float
+    residual: float
+    stepsize: float
+    block_hash: int
+    subspace_err: float | None = None
+
+
+class ConvergenceTrace:
+    COLUMNS = ("iter", "seconds", "passes", "residual", "stepsize", "subspace_err_l")
+
+    def __init__(self):
+        self.records = []
+        self._start = time.perf_counter()
+
+    def record(self, iteration, passes, residual, stepsize, block_hash, subspace_err=None):
+        self.records.append(TraceRecord(iteration, time.perf_counter() - self._start, passes,
+                                        residual, stepsize, block_hash, subspace_err))
+
+    def residuals(self):
+        return np.array([r.residual for r in self.records])
+
+    def passes(self):
+        return np.array([r.passes for r in self.records])
+
+    def final_residual(self):
+        for rec in reversed(self.records):
+            if np.isfinite(rec.residual):
+                return rec.residual
+        return math.nan
+
+    def passes_to(self, tol):
+        for rec in self.records:
+            if np.isfinite(rec.residual) and rec.residual <= tol:
+                return rec.passes
+        return math.inf
+
+    def to_csv(self, path):
+        with open(path, "w") as fh:
+            fh.write(",".join(self.COLUMNS) + "\n")
+            for r in self.records:
+                sub = "" if r.subspace_err is None else repr(r.subspace_err)
+                fh.write(f"{r.iteration},{r.seconds!r},{r.passes!r},{r.residual!r},"
+                         f"{r.stepsize!r},{sub}\n")
+
+
+class TailAverager:
+    """Streaming mean of iterates with indices in [ceil(T/2), T-1] (solvers.py:155-174)."""
+
+    def __init__(self, total_iters, shape):
+        if total_iters < 2:
+            raise ContractError("tail averaging needs at least two iterations")
+        self.start = math.ceil(total_iters / 2)
+        self.stop = total_iters - 1
+        self._sum = None
+        self.shape = shape
+        self.count = 0
+
+    def add(self, index, iterate):
+        if self.start <= index <= self.stop:
+            self._sum = iterate.clone() if self._sum is None else self._sum + iterate
+            self.count += 1
+
+    def average(self):
+        if self.count == 0:
+            raise ContractError("empty tail-average window")
+        return self._sum / self.count
+
+
+def tail_average(iterates):
+    items = list(iterates)
+    if not items:
+        raise ContractError("empty tail-average window")
+    total = np.zeros_like(np.asarray(items[0], dtype=np.float64))
+    for it in items:
+        total += it
+    return total / len(items)
+
+
+@dataclass
+class SolveResult:
+    W: np.ndarray
+    trace: ConvergenceTrace
+    diverged: bool
+    iterations: int
+    passes: float
+
+
+def resolve_blocksize(config, n):
+    b = config.blocksize if config.blocksize is not None else max(1, n // 100)
+    b = int(b)
+    if not 1 <= b <= n:
+        raise ConfigError(f"blocksize {b} outside [1, {n}]")
+    return b
+
+
+def resolve_rank(config, blocksize):
+    r = config.nystrom_rank if config.nystrom_rank is not None else min(100, blocksize)
+    r = int(r)
+    if not 1 <= r <= blocksize:
+        raise ConfigError(f"nystrom_rank {r} outside [1, {blocksize}]")
+    return r
+
+
+def budget_iterations(config, passes_per_iter):
+    if config.max_iters is not None:
+        return int(config.max_iters)
+    passes = config.max_passes if config.max_passes is not None else 50.0
+    return max(1, math.ceil(passes / passes_per_iter))
+
+
+def _due(every, t, total):
+    if every <= 0:
+        return t == total - 1
+    return (t + 1) % every == 0 or t == total - 1
+
+
+# ---------------------------------------------------------------------------
+# the engine
+
+
+def _basis(beta, alpha):
+    """Initial lazy basis: T's eigenvectors (1,1) and (1-beta, -alpha), unit norm.
+    Returns (M, dense_mode)."""
+    e2 = np.array([1.0 - beta, -alpha])
+    if abs(1.0 - beta + alpha) < 1e-12:
+        T = np.array([[beta, 1.0 - beta], [alpha, 1.0 - alpha]])
+        return np.eye(2), not np.array_equal(T, np.eye(2))
+    M = np.column_stack([np.ones(2) / math.sqrt(2.0), e2 / np.linalg.norm(e2)])
+    return M, False
+
+
+class SolverState:
+    """Iterate state of ADASAP. ``W``, ``V`` and ``Z`` materialise on demand
+    (numpy, float64) from the device-resident lazy form."""
+
+    def __init__(self, engine):
+        self._e = engine
+
+    @property
+    def iteration(self):
+        return self._e.t
+
+    @property
+    def W(self):
+        return self._e.materialize("W").cpu().numpy().astype(np.float64)
+
+    @property
+    def V(self):
+        return self._e.materialize("V").cpu().numpy().astype(np.float64)
+
+    @property
+    def Z(self):
+        return self._e.materialize("Z").cpu().numpy().astype(np.float64)
+
+
+class AdasapEngine:
+    """Device-resident ADASAP iteration (solvers.py:361-456)."""
+
+    def __init__(self, oracle, Y, config, accel, identity_precond=False, total=None, shard=None):
+        if not isinstance(oracle, KernelOracle):
+            raise ContractError("the B200 solver needs a device KernelOracle")
+        self.o = oracle
+        self.cfg = config
+        self.dev = oracle.device
+        n = oracle.n
+        self.n = n
+        self.shard = shard if shard is not None else current_shard(n)
+        Ya = Y if torch.is_tensor(Y) else np.asarray(Y, dtype=np.float64)
+        self.vector = Ya.ndim == 1
+        if Ya.shape[0] != n:
+            raise ContractError("right-hand side must have n rows")
+        Yl = Ya[self.shard.lo:self.shard.hi]
+        if Yl.ndim == 1:
+            Yl = Yl[:, None]
+        self.m = int(Ya.shape[1]) if Ya.ndim == 2 else 1
+        self.b = resolve_blocksize(config, n)
+        self.r = 0 if identity_precond else resolve_rank(config, self.b)
+        self.lam = oracle.lam
+        self.total = total if total is not None else budget_iterations(config, self.b / n)
+        beta, gamma, alpha = accel.beta, accel.gamma, accel.alpha
+        self.beta, self.gamma, self.alpha = beta, gamma, alpha
+        self.T = np.array([[beta, 1.0 - beta], [alpha, 1.0 - alpha]])
+        self.M, self.dense = _basis(beta, alpha)
+        self.M_prev = self.M.copy()
+        nl = self.shard.size
+        self.ld = max(4, (nl + 3) // 4 * 4)
+        f32 = torch.float32
+        self.P = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
+        self.Q = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
+        self.Y = to_colmajor(Yl, nl, self.dev, self.ld) if nl > 0 else \
+            torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
+        b, m = self.b, self.m
+        self.G = torch.empty((b, m), dtype=f32, device=self.dev)
+        self.g = torch.empty((b, m), dtype=torch.float64, device=self.dev)
+        self.WB = torch.zeros((b, m), dtype=f32, device=self.dev)
+        self.last_loc = None
+        self.etas = torch.zeros(max(self.total, 1), dtype=torch.float64, device=self.dev)
+        need = nat.load().sap_krows_workspace(b, m, max(nl, 1))
+        self.ws = torch.empty(max(need // 4 + 1, 1), dtype=f32, device=self.dev)
+        self.t = 0
+        self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
+                            config.lookahead, identity_precond)
+        self.crcs = []
+
+    def close(self):
+        self.la.close()
+
+    # -- one iteration ------------------------------------------------------------
+    def step(self, point=None):
+        """One ADASAP iteration; returns the host IterPlan (block, crc, rho)."""
+        plan = self.la.get(self.t)
+        sh = self.shard
+        zp, zq = self.M[1, 0], self.M[1, 1]
+        if point is None:
+            R, R2, ca, cb = self.P, self.Q, zp, zq
+        else:
+            R, R2, ca, cb = point, None, 1.0, 0.0
+        # Phase I: K[B, shard] Z[shard]
+        if sh.size > 0:
+            krows_times(self.o.spec, self.o.points, plan.Xb, plan.rsq, plan.block_dev, R,
+                        self.G, col_base=sh.lo, R2=R2, ca=ca, cb=cb, ws=self.ws, ncols=sh.size,
+                        col_offset=sh.lo)
+        else:
+            self.G.zero_()
+        gz = (zp, zq) if point is None else (1.0, 0.0)
+        gpoint = (self.P, self.Q) if point is None else (point, None)
+        nat.call("sap_grad_gather", nat.ptr(self.G), self.G.stride(0), nat.ptr(gpoint[0]),
+                 nat.ptr(gpoint[1]), nat.ptr(self.Y), self.ld, gz[0], gz[1],
+                 nat.ptr(plan.loc_dev), self.b, self.m, self.lam, nat.ptr(self.g),
+                 self.g.stride(0), nat.stream_handle())
+        allreduce_sum_(self.g)
+        # Phase IV: D_B = (g - U diag(Mc) U^T g) / rho
+        if plan.U is not None:
+            Utg = plan.U.T @ self.g
+            D = (self.g - plan.U @ (plan.Mc[:, None] * Utg)) / plan.rho
+        else:
+            D = self.g / plan.rho
+        self._update(plan, D)
+        self.etas[self.t:self.t + 1].copy_(plan.eta_dev)
+        self.last_loc = plan.loc_dev
+        self.crcs.append(plan.crc)
+        self.t += 1
+        return plan
+
+    def _update(self, plan, D):
+        beta, gamma, alpha = self.beta, self.gamma, self.alpha
+        delta = np.array([-gamma, -(1.0 - alpha)])
+        M = self.M
+        if self.dense:
+            # T != I with a defective eigenbasis: apply T to every row (rare configs)
+            self._pq(plan, D, M, 0.0, 0.0)
+            self.Wdense = self.Q[:, :self.shard.size].T.clone()  # Z_t: W_{t+1} off the block
+            P, Q = self.P.clone(), self.Q
+            self.P.mul_(beta).add_(Q, alpha=1.0 - beta)
+            self.Q.mul_(1.0 - alpha).add_(P, alpha=alpha)
+            self._pq(plan, D, M, delta[0], delta[1], wb=False)
+            self.M_prev = M
+            return
+        M_next = self.T @ M
+        e = np.linalg.solve(M_next, delta)
+        self._pq(plan, D, M, e[0], e[1])
+        self.M_prev, self.M = M, M_next
+        s = float(np.linalg.norm(M_next[:, 1]))
+        if s < RENORM_LO or s > RENORM_HI:
+            self.Q.mul_(s)
+            self.M = M_next.copy()
+            self.M[:, 1] /= s
+            self.M_prev = self.M_prev.copy()
+            self.M_prev[:, 1] /= s
+
+    def _pq(self, plan, D, M, e0, e1, wb=True):
+        nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
+                 nat.ptr(plan.loc_dev), self.b, self.m, nat.ptr(D), D.stride(0),
+                 nat.ptr(plan.eta_dev), M[1, 0], M[1, 1], e0, e1,
+                 nat.ptr(self.WB) if wb else None, self.WB.stride(0), nat.stream_handle())
+
+    # -- materialisation ------------------------------------------------------------
+    def materialize(self, which="W"):
+        """Local shard of W, V or Z as an (n_local x m) fp32 tensor."""
+        nl = self.shard.size
+        out = torch.empty((self.m, self.ld), dtype=torch.float32, device=self.dev)
+        if which == "W":
+            if self.t == 0:
+                return torch.zeros((nl, self.m), dtype=torch.float32, device=self.dev)
+            a, c = self.M_prev[1, 0], self.M_prev[1, 1]
+        elif which == "Z":
+            a, c = self.M[1, 0], self.M[1, 1]
+        else:
+            a, c = self.M[0, 0], self.M[0, 1]
+        if which == "W" and self.dense:
+            W = self.Wdense
+        else:
+            if nl > 0:
+                nat.call("sap_combine", nat.ptr(out), self.ld, nat.ptr(self.P), nat.ptr(self.Q),
+                         self.ld, nl, self.m, a, c, nat.stream_handle())
+            W = out[:, :nl].T
+        if which == "W":
+            loc = self.last_loc
+            own = loc >= 0
+            W = W.clone()
+            W[loc[own]] = self.WB[own]
+        return W
+
+    def gather_full(self, local):
+        """Concatenate shards (n x m) on every rank."""
+        if self.shard.world == 1:
+            return local
+        import torch.distributed as tdist
+        from .dist import partition
+        sizes = [hi - lo for lo, hi in partition(self.n, self.shard.world)]
+        mx = max(sizes)
+        buf = torch.zeros((mx, self.m), dtype=local.dtype, device=local.device)
+        buf[:local.shape[0]] = local
+        parts = [torch.empty_like(buf) for _ in sizes]
+        tdist.all_gather(parts, buf)
+        return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+
+    def relative_residual(self, W_local, ynorm):
+        """||K W + lam W - Y||_F / ||Y||_F over this shard's rows, summed over ranks
+        (solvers.py:254-257)."""
+        Wfull = self.gather_full(W_local)
+        Wcm = Wfull.T.contiguous()
+        sh = self.shard
+        if sh.size == 0:
+            part = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        else:
+            ids = torch.arange(sh.lo, sh.hi, device=self.dev, dtype=torch.int64)
+            Rs, rsq = self.o.points.Xs[sh.lo:sh.hi], self.o.points.sqn[sh.lo:sh.hi]
+            KW = torch.empty((sh.size, self.m), dtype=torch.float32, device=self.dev)
+            krows_times(self.o.spec, self.o.points, Rs, rsq, ids, Wcm, KW)
+            res = KW.double() + self.lam * W_local.double() - self.Y[:, :sh.size].T.double()
+            part = (res * res).sum().reshape(1)
+        allreduce_sum_(part)
+        return float(torch.sqrt(part)) / ynorm
+
+
+def _y_norm(Y):
+    Ya = Y if torch.is_tensor(Y) else np.asarray(Y, dtype=np.float64)
+    nrm = float(torch.linalg.vector_norm(Ya.double())) if torch.is_tensor(Ya) \
+        else float(np.linalg.norm(Ya))
+    return max(nrm, np.finfo(np.float64).tiny)
+
+
+def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=False):
+    """One iteration on an engine-backed state (solvers.py:361-403).
+
+    ``state`` is a SolverState returned by ``make_state``; returns
+    (state, eta, block) like the reference (eta read back from the device)."""
+    eng = state._e
+    plan = eng.step()
+    return state, float(eng.etas[eng.t - 1]), plan.block
+
+
+def make_state(oracle, Y, config, accel=None, identity_precond=False, total=None):
+    """Fresh zero state (solvers.py:197-202) bound to a device engine."""
+    n = oracle.n
+    b = resolve_blocksize(config, n)
+    if accel is None:
+        accel = resolve_accel(config, n, b)
+    eng = AdasapEngine(oracle, Y, config, accel, identity_precond, total)
+    return SolverState(eng)
+
+
+def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterate=None,
+                 accel=None):
+    """Accelerated approximate sketch-and-project from W0 = 0 (solvers.py:406-456)."""
+    n = oracle.n
+    config.validate_for(n)
+    b = resolve_blocksize(config, n)
+    if accel is None:
+        accel = resolve_accel(config, n, b)
+    total = budget_iterations(config, b / n)
+    eng = AdasapEngine(oracle, Y, config, accel, identity_precond, total)
+    try:
+        ynorm = _y_norm(Y)
+        trace = ConvergenceTrace()
+        averager = TailAverager(total, (n, eng.m)) if config.tail_average else None
+        diverged = False
+        done = 0
+        pending = []  # (iteration, passes, relres, crc) -- stepsizes filled at the end
+        for t in range(total):
+            point = eng.materialize("W").T.contiguous() if config.grad_eval_point == "w" and \
+                eng.t > 0 else None
+            if point is not None:
+                pt = torch.zeros((eng.m, eng.ld), dtype=torch.float32, device=eng.dev)
+                pt[:, :point.shape[1]] = point
+                point = pt
+            plan = eng.step(point)
+            done = t + 1
+            W_loc = None
+            if averager is not None or on_iterate is not None:
+                W_loc = eng.materialize("W")
+                if averager is not None:
+                    averager.add(done, W_loc)
+                if on_iterate is not None:
+                    on_iterate(done, eng.gather_full(W_loc).cpu().numpy().astype(np.float64))
+            relres = math.nan
+            if _due(config.residual_every, t, total):
+                W_loc = eng.materialize("W") if W_loc is None else W_loc
+                relres = eng.relative_residual(W_loc, ynorm)
+            trace.record(done, done * b / n, relres, math.nan, plan.crc)
+            if np.isfinite(relres):
+                finite = bool(torch.isfinite(W_loc).all())
+                if relres > DIVERGENCE_FACTOR or not finite:
+                    diverged = True
+                    break
+                if config.tol is not None and relres <= config.tol:
+                    break
+        eng.la.check_flags()
+        etas = eng.etas[:done].cpu().numpy()
+        for rec, eta in zip(trace.records, etas):
+            rec.stepsize = float(eta)
+        if averager is not None and averager.count > 0:
+            W_loc = averager.average()
+        else:
+            W_loc = eng.materialize("W")
+        W = eng.gather_full(W_loc).cpu().numpy().astype(np.float64)
+    finally:
+        eng.close()
+    return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)
+
+
+def solve(oracle, Y, config, dpp_model=None, pool=None, on_iterate=None):
+    """Dispatch on ``config.solver_id`` (solvers.py:591-615).
+
+    The B200 build implements the ADASAP hot path (``adasap``, ``adasap_i``);
+    the exact-SAP / SDD / PCG baselines are outside this build's scope."""
+    if config.solver_id == "adasap":
+        return adasap_solve(oracle, Y, config, on_iterate=on_iterate)
+    if config.solver_id == "adasap_i":
+        return adasap_solve(oracle, Y, config, identity_precond=True, on_iterate=on_iterate)
+    if config.solver_id in ("sap", "sdd", "pcg"):
+        raise ConfigError(f"solver {config.solver_id!r} is outside the B200 hot-path build")
+    raise ConfigError(f"unknown solver {config.solver_id!r}")

@@ -1,0 +1,125 @@
+"""Host-side logic of the drop-in API (no GPU): configuration parity with
+the reference, partitioning, index checks, and the algebra of the lazy
+two-array Nesterov state used by the engine."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2505_13723_b200 as sap
+from oracle import sapgp_oracle as orc
+from paper_2505_13723_b200 import dist, rng
+from paper_2505_13723_b200.parallel import ShardInfo
+from paper_2505_13723_b200.solvers import _basis, budget_iterations, resolve_blocksize
+
+
+def test_runconfig_defaults_and_validation():
+    c = sap.RunConfig()
+    assert (c.lam, c.max_passes, c.residual_every, c.grad_eval_point) == (1e-3, 50.0, 1, "z")
+    for bad in (dict(lam=0.0), dict(solver_id="x"), dict(grad_eval_point="q"), dict(seed=-1),
+                dict(max_passes=None), dict(mu=-1.0), dict(blocksize=0), dict(residual_every=-1)):
+        with pytest.raises(sap.ConfigError):
+            sap.RunConfig(**bad)
+    with pytest.raises(sap.ConfigError):
+        sap.RunConfig.from_dict({"lam": 1.0, "bogus": 1})
+    with pytest.raises(sap.ConfigError):
+        sap.RunConfig(blocksize=10).validate_for(5)
+    tree = sap.apply_overrides({}, ["run.lam=0.5", "run.tail_average=true", "kernel.family=rbf"])
+    assert tree == {"run": {"lam": 0.5, "tail_average": True}, "kernel": {"family": "rbf"}}
+    spec = sap.kernel_from_dict({"family": "matern32", "lengthscales": 2.0}, d=3)
+    assert spec.lengthscales.tolist() == [2.0, 2.0, 2.0]
+
+
+def test_budget_and_blocksize_defaults():
+    c = sap.RunConfig()
+    assert resolve_blocksize(c, 2000) == 20
+    assert budget_iterations(c, 200 / 2000) == 500
+
+
+def test_partition_matches_oracle():
+    for size in (0, 1, 5, 17, 257, 1000):
+        for parts in (1, 2, 3, 7):
+            assert dist.partition(size, parts) == orc.partition(size, parts)
+    assert dist.tile_ranges(1000) == orc.tile_ranges(1000)
+
+
+def test_check_indices():
+    for bad in ([], [0, 0], [-1], [10]):
+        with pytest.raises(sap.ContractError):
+            dist.check_indices(np.array(bad, dtype=np.int64), 10)
+
+
+def test_block_draws_match_reference_fixture():
+    from conftest import GOLDEN
+    import os
+    g = np.load(os.path.join(GOLDEN, "rng.npz"))
+    for seed, n, b, t, crc, first, last in g["rows"]:
+        blk = rng.uniform_block(seed, t, n, b)
+        assert rng.block_hash(blk) == crc and blk[0] == first and blk[-1] == last
+
+
+def _lazy_run(beta, gamma, alpha, steps=40, n=30, m=3, b=5, seed=0):
+    """Replay the engine's basis algebra in fp64 numpy and compare with the
+    dense recurrence of solvers.py:76-85."""
+    r = np.random.default_rng(seed)
+    W = np.zeros((n, m)); V = W.copy(); Z = W.copy()
+    P = np.zeros((n, m)); Q = np.zeros((n, m))
+    M, dense = _basis(beta, alpha)
+    assert not dense
+    T = np.array([[beta, 1 - beta], [alpha, 1 - alpha]])
+    delta = np.array([-gamma, -(1 - alpha)])
+    for _ in range(steps):
+        B = np.sort(r.choice(n, b, replace=False))
+        D = np.zeros((n, m)); D[B] = r.standard_normal((b, m))
+        eta = r.uniform(0.1, 1.0)
+        W, V, Z = orc.nesterov_update(W, V, Z, D, eta, beta, gamma, alpha)
+        Zt = M[1, 0] * P + M[1, 1] * Q
+        WB = Zt[B] - eta * D[B]
+        Mn = T @ M
+        e = np.linalg.solve(Mn, delta)
+        P[B] += e[0] * eta * D[B]
+        Q[B] += e[1] * eta * D[B]
+        Wl = M[1, 0] * P + M[1, 1] * Q
+        Wl[B] = WB
+        M = Mn
+        s = np.linalg.norm(M[:, 1])
+        if s < 2.0 ** -20:
+            Q *= s; M[:, 1] /= s
+        Vl = M[0, 0] * P + M[0, 1] * Q
+        Zl = M[1, 0] * P + M[1, 1] * Q
+        sc = max(1.0, np.abs(Z).max())
+        assert np.abs(Wl - W).max() <= 1e-10 * sc
+        assert np.abs(Vl - V).max() <= 1e-10 * sc
+        assert np.abs(Zl - Z).max() <= 1e-10 * sc
+
+
+def test_lazy_nesterov_basis_reproduces_dense_update():
+    co = orc.accel_coeffs(1e-2, 1_000_000, 2000)
+    _lazy_run(*co)
+    _lazy_run(*orc.accel_coeffs(0.3, 40, 8))
+    _lazy_run(*orc.accel_coeffs(1e-3, 200, 2), steps=3000)  # exercises renormalisation
+
+
+def test_identity_accel_uses_trivial_basis():
+    M, dense = _basis(1.0, 0.0)
+    assert np.array_equal(M, np.eye(2)) and not dense
+
+
+def test_shard_info():
+    for n in (1, 7, 1000):
+        for world in (1, 2, 3, 8):
+            shards = [ShardInfo.of(n, r, world) for r in range(world)]
+            assert shards[0].lo == 0 and shards[-1].hi == n
+            assert sum(s.size for s in shards) == n
+            blk = np.arange(n)
+            owners = sum((s.local_positions(blk) >= 0).astype(int) for s in shards)
+            assert np.all(owners == 1)
+
+
+def test_no_cpu_fallback_without_device(monkeypatch):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    with pytest.raises(sap.WorkerError):
+        sap.KernelOracle(sap.KernelSpec("rbf", np.ones(2)), np.zeros((4, 2)), 0.1)
