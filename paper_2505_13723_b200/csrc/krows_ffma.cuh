@@ -48,7 +48,8 @@ struct KrowsParams {
 };
 
 template <int FAM, int DP, int MT>
-__global__ void __launch_bounds__(kFfmaThreads, 1) krows_ffma_kernel(const KrowsParams p) {
+__global__ void __launch_bounds__(kFfmaThreads, (MT <= 5 && DP <= 16) ? 2 : 1)
+    krows_ffma_kernel(const KrowsParams p) {
   constexpr int MC = 16 * MT;
   constexpr int MCP = MC + 1;
   constexpr int XV = kFfmaBN * DP / 4;                 // float4 per column-coord tile

@@ -183,11 +183,20 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float *out, int iters) {
 constexpr int kTargetCtas = 2 * 148;  // a pure function of the shape: deterministic
 
 int pick_splits(int64_t b, int m, int64_t tiles) {
+  // Choose the column split so the grid fills whole waves of 2 CTAs per SM
+  // (148 SMs); a pure function of the shape, so results are deterministic.
   const int64_t row_tiles = (b + kFfmaBM - 1) / kFfmaBM;
-  const int64_t m_chunks = (m + 127) / 128;
-  int64_t s = (kTargetCtas + row_tiles * m_chunks - 1) / (row_tiles * m_chunks);
-  s = std::min<int64_t>(s, std::max<int64_t>(1, tiles / 8));
-  return int(std::max<int64_t>(1, std::min<int64_t>(s, 1024)));
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(tiles / 8, 4096));
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t s = 1; s <= std::min<int64_t>(max_s, 4 * kTargetCtas); ++s) {
+    const int64_t total = row_tiles * s;
+    const int64_t waves = (total + kTargetCtas - 1) / kTargetCtas;
+    if (waves > 4) break;
+    const double eff = double(total) / double(waves * kTargetCtas);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return int(best);
 }
 
 int launch_ffma_rbf(KrowsParams p, int dp, cudaStream_t st);

@@ -233,14 +233,21 @@ def _due(every, t, total):
 
 
 def _basis(beta, alpha):
-    """Initial lazy basis: T's eigenvectors (1,1) and (1-beta, -alpha), unit norm.
-    Returns (M, dense_mode)."""
+    """Eigen-directions of T = [[beta, 1-beta], [alpha, 1-alpha]] for the lazy state.
+
+    T has eigenvalue 1 on u1 = (1, 1)/sqrt(2) and lam2 = beta - alpha on
+    u2 = (1-beta, -alpha)/|.|. The basis at iteration t is M_t = [u1, s_t u2]
+    with the scalar recurrence s_{t+1} = lam2 s_t, so the directions never
+    accumulate rounding (propagating M <- T M would let u2 drift into u1).
+    Returns (u1, u2, lam2, dense); ``dense`` marks defective / degenerate T."""
+    T = np.array([[beta, 1.0 - beta], [alpha, 1.0 - alpha]])
+    if np.array_equal(T, np.eye(2)):
+        return np.array([1.0, 0.0]), np.array([0.0, 1.0]), 1.0, False
+    lam2 = beta - alpha
     e2 = np.array([1.0 - beta, -alpha])
-    if abs(1.0 - beta + alpha) < 1e-12:
-        T = np.array([[beta, 1.0 - beta], [alpha, 1.0 - alpha]])
-        return np.eye(2), not np.array_equal(T, np.eye(2))
-    M = np.column_stack([np.ones(2) / math.sqrt(2.0), e2 / np.linalg.norm(e2)])
-    return M, False
+    if abs(1.0 - beta + alpha) < 1e-12 or abs(lam2) < 1e-6:
+        return np.array([1.0, 0.0]), np.array([0.0, 1.0]), 1.0, True
+    return np.ones(2) / math.sqrt(2.0), e2 / np.linalg.norm(e2), lam2, False
 
 
 class SolverState:
@@ -293,9 +300,8 @@ class AdasapEngine:
         self.total = total if total is not None else budget_iterations(config, self.b / n)
         beta, gamma, alpha = accel.beta, accel.gamma, accel.alpha
         self.beta, self.gamma, self.alpha = beta, gamma, alpha
-        self.T = np.array([[beta, 1.0 - beta], [alpha, 1.0 - alpha]])
-        self.M, self.dense = _basis(beta, alpha)
-        self.M_prev = self.M.copy()
+        self.u1, self.u2, self.lam2, self.dense = _basis(beta, alpha)
+        self.s = self.s_prev = 1.0
         nl = self.shard.size
         self.ld = max(4, (nl + 3) // 4 * 4)
         f32 = torch.float32
@@ -356,31 +362,36 @@ class AdasapEngine:
         self.t += 1
         return plan
 
+    @property
+    def M(self):
+        return np.column_stack([self.u1, self.s * self.u2])
+
+    @property
+    def M_prev(self):
+        return np.column_stack([self.u1, self.s_prev * self.u2])
+
     def _update(self, plan, D):
         beta, gamma, alpha = self.beta, self.gamma, self.alpha
         delta = np.array([-gamma, -(1.0 - alpha)])
         M = self.M
         if self.dense:
-            # T != I with a defective eigenbasis: apply T to every row (rare configs)
+            # degenerate T (repeated/zero second eigenvalue): apply T to every row
             self._pq(plan, D, M, 0.0, 0.0)
             self.Wdense = self.Q[:, :self.shard.size].T.clone()  # Z_t: W_{t+1} off the block
-            P, Q = self.P.clone(), self.Q
-            self.P.mul_(beta).add_(Q, alpha=1.0 - beta)
+            P = self.P.clone()
+            self.P.mul_(beta).add_(self.Q, alpha=1.0 - beta)
             self.Q.mul_(1.0 - alpha).add_(P, alpha=alpha)
             self._pq(plan, D, M, delta[0], delta[1], wb=False)
-            self.M_prev = M
             return
-        M_next = self.T @ M
+        s_next = self.lam2 * self.s
+        M_next = np.column_stack([self.u1, s_next * self.u2])
         e = np.linalg.solve(M_next, delta)
         self._pq(plan, D, M, e[0], e[1])
-        self.M_prev, self.M = M, M_next
-        s = float(np.linalg.norm(M_next[:, 1]))
-        if s < RENORM_LO or s > RENORM_HI:
-            self.Q.mul_(s)
-            self.M = M_next.copy()
-            self.M[:, 1] /= s
-            self.M_prev = self.M_prev.copy()
-            self.M_prev[:, 1] /= s
+        self.s_prev, self.s = self.s, s_next
+        if abs(s_next) < RENORM_LO or abs(s_next) > RENORM_HI:
+            self.Q.mul_(s_next)
+            self.s_prev /= s_next
+            self.s = 1.0
 
     def _pq(self, plan, D, M, e0, e1, wb=True):
         nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
