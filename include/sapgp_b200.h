@@ -24,6 +24,9 @@
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
+ *   sap_krows_tc (+ sap_tc_points, sap_tc_gather_rows, sap_z_operand)
+ *                       <- the same col_dist_matmul product on the 5th-gen
+ *                          tensor cores (the solver's Phase I, solvers.py:377)
  *
  * Layouts (all row/column strides in elements):
  *   point set   Xs[j*ldx + k] float32, scaled by 1/lengthscale, zero padded
@@ -108,16 +111,58 @@ int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q,
  * Block-row Nesterov step in the lazy basis: for owned rows
  *   WB[i, c] = Z[j, c] - eta * D[i, c]          (Z = zp*P + zq*Q, old basis)
  *   P[j, c] += e0 * eta * D[i, c];  Q[j, c] += e1 * eta * D[i, c]
- * eta is read from device memory (eta_dev[0]).
+ * eta is read from device memory (eta_dev[0]). Pb/Qb (nullable) are per-column
+ * magnitude bounds, raised (atomicMax) to cover the updated values.
  */
 int sap_pq_update(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b, int m,
                   const double *D, int64_t ldd, const double *eta_dev,
                   double zp, double zq, double e0, double e1,
-                  float *WB, int64_t ldwb, void *stream);
+                  float *WB, int64_t ldwb, float *Pb, float *Qb, void *stream);
 
 /* out = a*P + b*Q (column-major n x m, ld ldp); Q may be NULL (b ignored). */
 int sap_combine(float *out, int64_t ldo, const float *P, const float *Q, int64_t ldp,
                 int64_t n, int m, double a, double b, void *stream);
+
+/* ---- tensor-core path (krows_tc.cu) ------------------------------------ */
+
+/*
+ * Augmented features for the 3-term tf32 distance GEMM (ka = 32 for d <= 9,
+ * 64 for d <= 20): row form RA[j*ka..] and/or column form CA[j*ka..]
+ * (either may be NULL), scaled by sqrt(c_family)/lengthscale.
+ */
+int sap_tc_points(const double *X, int64_t n, int d, const double *inv_ls, int family, int ka,
+                  float *RA, float *CA, void *stream);
+
+/* out[i*ka..] = RA[idx[i]*ka..] for i < b, zero rows for b <= i < bpad. */
+int sap_tc_gather_rows(const float *RA, int ka, const int64_t *idx, int64_t b, int64_t bpad,
+                       float *out, void *stream);
+
+/*
+ * Z operand of the tensor-core product: Zhi/Zlo (fp16, [nz][ldz]) = split of
+ * scale_c * (zp*P + zq*Q) with scale_c a power of two from the bounds Pb/Qb
+ * (zscale[c] receives it). Q/Qb may be NULL.
+ */
+int sap_z_operand(const float *P, const float *Q, int64_t ldp, int64_t n, int m, double zp,
+                  double zq, const float *Pb, const float *Qb, int nz, int64_t ldz, void *Zhi,
+                  void *Zlo, float *zscale, void *stream);
+
+/* out[c] = max_j |A[c*lda + j]| (bounds for RHS that are not solver state). */
+int sap_colabsmax(const float *A, int64_t lda, int64_t n, int m, float *out, void *stream);
+
+size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols);
+
+/*
+ * Tensor-core block-row product (tcgen05 + TMEM + TMA, sm_100a):
+ * out[i, c] (=, or +=) variance * sum_j k(row_i, col_j) Z[j, c] with rows
+ * RAg ([bpad][ka], bpad a multiple of 128), columns CA ([ncols][ka]) and Z
+ * given by sap_z_operand. Diagonal rule as sap_krows_times (row_ids vs
+ * col_base + j). nz <= 128.
+ */
+int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64_t bpad,
+                 const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
+                 const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
+                 double variance, float *out, int64_t ldo, int accumulate, void *ws,
+                 size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

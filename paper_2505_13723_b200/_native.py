@@ -42,8 +42,15 @@ SIGNATURES = {
     "sap_ktile": (_I, [_P, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _I, _D, _P, _I64, _P]),
     "sap_grad_gather": (_I, [_P, _I64, _P, _P, _P, _I64, _D, _D, _P, _I64, _I, _D, _P, _I64, _P]),
     "sap_pq_update": (_I, [_P, _P, _I64, _P, _I64, _I, _P, _I64, _P, _D, _D, _D, _D, _P, _I64,
-                           _P]),
+                           _P, _P, _P]),
     "sap_combine": (_I, [_P, _I64, _P, _P, _I64, _I64, _I, _D, _D, _P]),
+    "sap_tc_points": (_I, [_P, _I64, _I, _P, _I, _I, _P, _P, _P]),
+    "sap_tc_gather_rows": (_I, [_P, _I, _P, _I64, _I64, _P, _P]),
+    "sap_z_operand": (_I, [_P, _P, _I64, _I64, _I, _D, _D, _P, _P, _I, _I64, _P, _P, _P, _P]),
+    "sap_colabsmax": (_I, [_P, _I64, _I64, _I, _P, _P]),
+    "sap_krows_tc_workspace": (_SZ, [_I64, _I, _I64]),
+    "sap_krows_tc": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I64, _P, _P, _I, _I64, _P, _I, _I, _D,
+                          _P, _I64, _I, _P, _SZ, _P]),
 }
 
 _lib = None

@@ -115,7 +115,7 @@ __global__ void grad_gather_kernel(const float *G, int64_t ldg, const float *P, 
 __global__ void pq_update_kernel(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b,
                                  int m, const double *D, int64_t ldd, const double *eta_dev,
                                  double zp, double zq, double e0, double e1, float *WB,
-                                 int64_t ldwb) {
+                                 int64_t ldwb, float *Pb, float *Qb) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= b * m) return;
   const int64_t i = e / m;
@@ -128,8 +128,14 @@ __global__ void pq_update_kernel(float *P, float *Q, int64_t ldp, const int64_t 
   const double p = P[o];
   const double q = Q ? double(Q[o]) : 0.0;
   if (WB) WB[i * ldwb + c] = float(zp * p + zq * q - eta * dd);
-  P[o] = float(p + e0 * eta * dd);
-  if (Q) Q[o] = float(q + e1 * eta * dd);
+  const float pn = float(p + e0 * eta * dd);
+  P[o] = pn;
+  if (Pb) atomicMax(reinterpret_cast<int *>(Pb + c), __float_as_int(fabsf(pn)));
+  if (Q) {
+    const float qn = float(q + e1 * eta * dd);
+    Q[o] = qn;
+    if (Qb) atomicMax(reinterpret_cast<int *>(Qb + c), __float_as_int(fabsf(qn)));
+  }
 }
 
 __global__ void combine_kernel(float *out, int64_t ldo, const float *P, const float *Q,
@@ -355,11 +361,12 @@ int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q,
 
 int sap_pq_update(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b, int m,
                   const double *D, int64_t ldd, const double *eta_dev, double zp, double zq,
-                  double e0, double e1, float *WB, int64_t ldwb, void *stream) {
+                  double e0, double e1, float *WB, int64_t ldwb, float *Pb, float *Qb,
+                  void *stream) {
   if (b <= 0 || m <= 0) return fail(SAP_ERR_CONTRACT, "pq_update: bad shape");
   const int64_t tot = b * m;
   pq_update_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
-      P, Q, ldp, loc, b, m, D, ldd, eta_dev, zp, zq, e0, e1, WB, ldwb);
+      P, Q, ldp, loc, b, m, D, ldd, eta_dev, zp, zq, e0, e1, WB, ldwb, Pb, Qb);
   return check_launch("pq_update_kernel");
 }
 

@@ -134,6 +134,79 @@ def krows_times(spec, cols, Rs, rsq, row_ids, R, out, col_ids=None, col_base=0, 
     return out
 
 
+class TcPoints:
+    """Augmented features of the tensor-core path (krows_tc.cu): row form RA
+    for every point (rows are gathered per block) and column form CA for the
+    points of one shard [lo, hi)."""
+
+    def __init__(self, spec, X, device, lo=0, hi=None):
+        Xd = torch.as_tensor(np.asarray(X, dtype=np.float64) if not torch.is_tensor(X) else X,
+                             dtype=torch.float64).to(device).contiguous()
+        n, d = Xd.shape
+        hi = n if hi is None else hi
+        self.ka = 32 if 3 * d + 4 <= 32 else 64
+        if 3 * d + 4 > 64:
+            raise ContractError(f"tensor-core path supports d <= 20 (got d={d})")
+        inv = torch.as_tensor(np.broadcast_to(1.0 / spec.lengthscales, (d,)).copy(), device=device)
+        self.RA = torch.empty((max(n, 1), self.ka), dtype=torch.float32, device=device)
+        self.CA = torch.empty((max(hi - lo, 1), self.ka), dtype=torch.float32, device=device)
+        with torch.cuda.device(device):
+            nat.call("sap_tc_points", nat.ptr(Xd), n, d, nat.ptr(inv), spec.code, self.ka,
+                     nat.ptr(self.RA), None, nat.stream_handle())
+            if hi > lo:
+                nat.call("sap_tc_points", nat.ptr(Xd[lo:hi]), hi - lo, d, nat.ptr(inv), spec.code,
+                         self.ka, None, nat.ptr(self.CA), nat.stream_handle())
+        self.lo, self.hi, self.n, self.d, self.device = lo, hi, n, d, device
+
+    def gather_rows(self, idx_dev, out=None):
+        b = idx_dev.numel()
+        bpad = (b + 127) // 128 * 128
+        if out is None:
+            out = torch.empty((bpad, self.ka), dtype=torch.float32, device=self.device)
+        nat.call("sap_tc_gather_rows", nat.ptr(self.RA), self.ka, nat.ptr(idx_dev), b, bpad,
+                 nat.ptr(out), nat.stream_handle())
+        return out
+
+
+class ZOperand:
+    """fp16 hi/lo split of a (scaled) RHS in the tensor-core B layout [nz][ldz]."""
+
+    def __init__(self, m, n, device):
+        self.m, self.n = m, n
+        self.nz = (m + 15) // 16 * 16
+        if self.nz > 128:
+            raise ContractError("tensor-core path supports at most 128 right-hand sides")
+        self.ldz = max(8, (n + 7) // 8 * 8)
+        self.hi = torch.empty((self.nz, self.ldz), dtype=torch.float16, device=device)
+        self.lo = torch.empty((self.nz, self.ldz), dtype=torch.float16, device=device)
+        self.scale = torch.ones(self.nz, dtype=torch.float32, device=device)
+        self.bound = torch.zeros(self.nz, dtype=torch.float32, device=device)
+
+    def fill(self, P, Q=None, zp=1.0, zq=0.0, Pb=None, Qb=None):
+        """Z = zp P + zq Q (column-major fp32, m x ld); bounds computed if not given."""
+        if Pb is None:
+            nat.call("sap_colabsmax", nat.ptr(P), P.stride(0), self.n, self.m, nat.ptr(self.bound),
+                     nat.stream_handle())
+            Pb, Q, Qb, zq = self.bound, None, None, 0.0
+        nat.call("sap_z_operand", nat.ptr(P), nat.ptr(Q), P.stride(0), self.n, self.m, zp, zq,
+                 nat.ptr(Pb), nat.ptr(Qb), self.nz, self.ldz, nat.ptr(self.hi), nat.ptr(self.lo),
+                 nat.ptr(self.scale), nat.stream_handle())
+        return self
+
+
+def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False):
+    """out (b x m fp32) = variance * K(rows, shard columns) @ Z on the tensor cores."""
+    ncols = tcp.hi - tcp.lo
+    need = nat.load().sap_krows_tc_workspace(b, zop.m, ncols)
+    if ws is None or ws.numel() * 4 < need:
+        ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=tcp.device)
+    nat.call("sap_krows_tc", nat.ptr(tcp.CA), ncols, tcp.ka, nat.ptr(RAg), RAg.shape[0],
+             nat.ptr(row_ids), b, tcp.lo, nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz,
+             nat.ptr(zop.scale), zop.m, spec.code, spec.variance, nat.ptr(out), out.stride(0),
+             int(accumulate), nat.ptr(ws), ws.numel() * 4, nat.stream_handle())
+    return out
+
+
 def ktile(spec, A, asq, aid, C, csq, cid, ldx, d):
     out = torch.empty((A.shape[0], C.shape[0]), dtype=torch.float64, device=A.device)
     nat.call("sap_ktile", nat.ptr(A), nat.ptr(asq), nat.ptr(aid), A.shape[0], nat.ptr(C),
@@ -185,6 +258,22 @@ class KernelOracle:
         self.device = _device(device)
         self.points = DevicePoints(spec, Xn, self.device)
         self._ws = None
+        self._tc = None
+        self.backend = "auto"  # "tc" (tcgen05), "ffma", or "auto" (tc when the shape fits)
+
+    def tc_points(self, lo=0, hi=None):
+        hi = self.n if hi is None else hi
+        if self._tc is None or (self._tc.lo, self._tc.hi) != (lo, hi):
+            self._tc = TcPoints(self.spec, self.X, self.device, lo, hi)
+        return self._tc
+
+    def use_tc(self, m):
+        if self.backend == "ffma":
+            return False
+        fits = 3 * self.d + 4 <= 64 and m <= 128
+        if self.backend == "tc" and not fits:
+            raise ContractError("shape outside the tensor-core path (d <= 20, m <= 128)")
+        return fits
 
     @property
     def n(self):
@@ -234,9 +323,23 @@ class KernelOracle:
     def rows_times_device(self, block_dev, Rcm, out=None, R2=None, ca=1.0, cb=0.0):
         """K[block, :] @ R for a column-major device RHS; fp32 (b x m) out."""
         b, m = block_dev.numel(), Rcm.shape[0]
-        Rs, rsq = self.points.gather(block_dev)
         if out is None:
             out = torch.empty((b, m), dtype=torch.float32, device=self.device)
+        if self.use_tc(m) and b >= 16:
+            tcp = self.tc_points()
+            zop = ZOperand(m, self.n, self.device)
+            if R2 is None:
+                zop.fill(Rcm, zp=ca)
+            else:
+                b1 = torch.zeros(zop.nz, dtype=torch.float32, device=self.device)
+                b2 = torch.zeros(zop.nz, dtype=torch.float32, device=self.device)
+                nat.call("sap_colabsmax", nat.ptr(Rcm), Rcm.stride(0), self.n, m, nat.ptr(b1),
+                         nat.stream_handle())
+                nat.call("sap_colabsmax", nat.ptr(R2), R2.stride(0), self.n, m, nat.ptr(b2),
+                         nat.stream_handle())
+                zop.fill(Rcm, R2, ca, cb, b1, b2)
+            return krows_tc(self.spec, tcp, tcp.gather_rows(block_dev), b, block_dev, zop, out)
+        Rs, rsq = self.points.gather(block_dev)
         return krows_times(self.spec, self.points, Rs, rsq, block_dev, Rcm, out, R2=R2, ca=ca,
                            cb=cb, ws=self._workspace(b, m, self.n))
 

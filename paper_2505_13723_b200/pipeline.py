@@ -50,10 +50,11 @@ class IterPlan:
     rho: float
     eta_dev: torch.Tensor      # (1,) fp64 view
     S: np.ndarray
+    RAg: torch.Tensor | None = None  # (bpad, ka) gathered tensor-core row features
 
 
 class _Slot:
-    def __init__(self, L, b, r, ldx, dev):
+    def __init__(self, L, b, r, ldx, dev, ka=0):
         f32, f64, i64 = torch.float32, torch.float64, torch.int64
         self.block_dev = torch.empty((L, b), dtype=i64, device=dev)
         self.loc_dev = torch.empty((L, b), dtype=i64, device=dev)
@@ -63,6 +64,8 @@ class _Slot:
         self.Mc = torch.empty((L, r), dtype=f64, device=dev) if r else None
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
+        bpad = (b + 127) // 128 * 128
+        self.RAg = torch.empty((L, bpad, ka), dtype=f32, device=dev) if ka else None
         pin = torch.cuda.is_available()
         self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
         self.h_omega = torch.empty((L, b, max(r, 1)), dtype=f64, pin_memory=pin)
@@ -90,7 +93,8 @@ class _Batch:
 class Lookahead:
     """Produces IterPlan(t) for t = 0..total-1 in batches of ``L``."""
 
-    def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10):
+    def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
+                 tcp=None):
         self.o, self.shard, self.seed = oracle, shard, seed
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
         self.total, self.L = total, max(1, min(L, total))
@@ -98,7 +102,9 @@ class Lookahead:
         dev = oracle.device
         self.dev = dev
         self.side = torch.cuda.Stream(device=dev)
-        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev) for _ in range(2)]
+        self.tcp = tcp
+        ka = tcp.ka if tcp is not None else 0
+        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(2)]
         self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sap-lookahead")
         self.cur = None
         self.k = 0
@@ -130,7 +136,8 @@ class Lookahead:
             t=t, block=cur.blocks[i], crc=cur.crcs[i], block_dev=s.block_dev[i],
             loc_dev=s.loc_dev[i], Xb=s.Xb[i], rsq=s.rsq[i],
             U=None if s.U is None else s.U[i], Mc=None if s.Mc is None else s.Mc[i],
-            rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i])
+            rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i],
+            RAg=None if s.RAg is None else s.RAg[i])
 
     def check_flags(self):
         """Raise if any power iteration failed (checked once, at the end)."""
@@ -178,6 +185,8 @@ class Lookahead:
             sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
             for i in range(count):
                 Xb, rsq = pts.gather(bd[i], out=(slot.Xb[i], slot.rsq[i]))
+                if self.tcp is not None:
+                    self.tcp.gather_rows(bd[i], out=slot.RAg[i])
                 Kbb[i] = K.ktile(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d)
                 if r:
                     omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS

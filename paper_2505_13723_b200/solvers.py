@@ -42,7 +42,7 @@ import torch
 from . import _native as nat
 from .dist import WorkerPool
 from .errors import ConfigError, ContractError
-from .kernels import KernelOracle, krows_times, to_colmajor
+from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
 from .parallel import ShardInfo, allreduce_sum_, current_shard
 from .pipeline import Lookahead
 from .rng import block_hash
@@ -315,11 +315,20 @@ class AdasapEngine:
         self.WB = torch.zeros((b, m), dtype=f32, device=self.dev)
         self.last_loc = None
         self.etas = torch.zeros(max(self.total, 1), dtype=torch.float64, device=self.dev)
-        need = nat.load().sap_krows_workspace(b, m, max(nl, 1))
+        self.use_tc = oracle.use_tc(m) and b >= 16 and nl > 0 and not self.dense
+        if self.use_tc:
+            self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi)
+            self.zop = ZOperand(m, nl, self.dev)
+            self.Pb = torch.zeros(self.zop.nz, dtype=f32, device=self.dev)
+            self.Qb = torch.zeros(self.zop.nz, dtype=f32, device=self.dev)
+            need = nat.load().sap_krows_tc_workspace(b, m, nl)
+        else:
+            self.tcp = self.zop = self.Pb = self.Qb = None
+            need = nat.load().sap_krows_workspace(b, m, max(nl, 1))
         self.ws = torch.empty(max(need // 4 + 1, 1), dtype=f32, device=self.dev)
         self.t = 0
         self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
-                            config.lookahead, identity_precond)
+                            config.lookahead, identity_precond, tcp=self.tcp)
         self.crcs = []
 
     def close(self):
@@ -336,7 +345,14 @@ class AdasapEngine:
         else:
             R, R2, ca, cb = point, None, 1.0, 0.0
         # Phase I: K[B, shard] Z[shard]
-        if sh.size > 0:
+        if sh.size > 0 and self.use_tc:
+            if point is None:
+                self.zop.fill(self.P, self.Q, zp, zq, self.Pb, self.Qb)
+            else:
+                self.zop.fill(point)
+            krows_tc(self.o.spec, self.tcp, plan.RAg, self.b, plan.block_dev, self.zop, self.G,
+                     ws=self.ws)
+        elif sh.size > 0:
             krows_times(self.o.spec, self.o.points, plan.Xb, plan.rsq, plan.block_dev, R,
                         self.G, col_base=sh.lo, R2=R2, ca=ca, cb=cb, ws=self.ws, ncols=sh.size,
                         col_offset=sh.lo)
@@ -390,6 +406,8 @@ class AdasapEngine:
         self.s_prev, self.s = self.s, s_next
         if abs(s_next) < RENORM_LO or abs(s_next) > RENORM_HI:
             self.Q.mul_(s_next)
+            if self.Qb is not None:
+                self.Qb.mul_(abs(s_next))
             self.s_prev /= s_next
             self.s = 1.0
 
@@ -397,7 +415,8 @@ class AdasapEngine:
         nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
                  nat.ptr(plan.loc_dev), self.b, self.m, nat.ptr(D), D.stride(0),
                  nat.ptr(plan.eta_dev), M[1, 0], M[1, 1], e0, e1,
-                 nat.ptr(self.WB) if wb else None, self.WB.stride(0), nat.stream_handle())
+                 nat.ptr(self.WB) if wb else None, self.WB.stride(0), nat.ptr(self.Pb),
+                 nat.ptr(self.Qb), nat.stream_handle())
 
     # -- materialisation ------------------------------------------------------------
     def materialize(self, which="W"):
