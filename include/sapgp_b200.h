@@ -151,6 +151,9 @@ int sap_colabsmax(const float *A, int64_t lda, int64_t n, int m, float *out, voi
 
 size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols);
 
+/* 1 if (d features, m right-hand sides) fits the tensor-core path, else 0. */
+int sap_tc_supported(int d, int m);
+
 /*
  * Tensor-core block-row product (tcgen05 + TMEM + TMA, sm_100a):
  * out[i, c] (=, or +=) variance * sum_j k(row_i, col_j) Z[j, c] with rows

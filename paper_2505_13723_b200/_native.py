@@ -49,6 +49,7 @@ SIGNATURES = {
     "sap_z_operand": (_I, [_P, _P, _I64, _I64, _I, _D, _D, _P, _P, _I, _I64, _P, _P, _P, _P]),
     "sap_colabsmax": (_I, [_P, _I64, _I64, _I, _P, _P]),
     "sap_krows_tc_workspace": (_SZ, [_I64, _I, _I64]),
+    "sap_tc_supported": (_I, [_I, _I]),
     "sap_krows_tc": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I64, _P, _P, _I, _I64, _P, _I, _I, _D,
                           _P, _I64, _I, _P, _SZ, _P]),
 }

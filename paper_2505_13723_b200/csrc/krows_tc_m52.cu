@@ -1,0 +1,12 @@
+// Tensor-core block-row kernel instantiated for one covariance family.
+#include "krows_tc.cuh"
+
+namespace sap {
+namespace tck {
+bool launch_tc_m52(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
+                    const CUtensorMap &zl, const Params &p, int nz, int ka, int grid,
+                    cudaStream_t st) {
+  return launch_tc_family<SAP_MATERN52>(a, c, zh, zl, p, nz, ka, grid, st);
+}
+}  // namespace tck
+}  // namespace sap

@@ -270,7 +270,7 @@ class KernelOracle:
     def use_tc(self, m):
         if self.backend == "ffma":
             return False
-        fits = 3 * self.d + 4 <= 64 and m <= 128
+        fits = bool(nat.load().sap_tc_supported(self.d, m))
         if self.backend == "tc" and not fits:
             raise ContractError("shape outside the tensor-core path (d <= 20, m <= 128)")
         return fits

@@ -15,9 +15,11 @@ ap.add_argument("--b", type=int, default=2000)
 ap.add_argument("--m", type=int, default=65)
 ap.add_argument("--d", type=int, default=9)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--backend", default="tc")
 a = ap.parse_args()
 X = synthetic.make_inputs(a.n, a.d, 0)
 o = sap.KernelOracle(sap.KernelSpec(a.family, np.full(a.d, np.sqrt(a.d)), 1.0), X, 1e-2)
+o.backend = a.backend
 Z = torch.randn(a.m, a.n, device="cuda")
 B = torch.as_tensor(np.sort(np.random.default_rng(0).choice(a.n, a.b, replace=False)), device="cuda")
 out = torch.empty(a.b, a.m, device="cuda")
