@@ -39,6 +39,10 @@ sys.path.insert(0, ROOT)
 for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
     os.environ.setdefault(_v, "1")
 
+# dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at this
+# config, from the committed ncu capture (profiles/); None until captured.
+TRAFFIC_PER_LAUNCH = None
+
 CONFIG = dict(n=1_000_000, d=9, family="matern32", b=2000, m=65, r=100, lam=1e-2, seed=0)
 METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target RMSE"
 
@@ -197,21 +201,23 @@ def run_b200(args):
         eng.step()
     torch.cuda.synchronize()
 
-    # kernel-level events around the dominant launch (same stream)
-    from paper_2505_13723_b200 import kernels as K
-    orig = K.krows_times
-    evs = []
-
-    def timed_krows(*a, **kw):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        out = orig(*a, **kw)
-        e.record()
-        evs.append((s, e))
-        return out
-
+    # kernel-level events around the dominant launch (same stream as the launch)
     import paper_2505_13723_b200.solvers as S
-    S.krows_times = timed_krows
+    evs = []
+    originals = {name: getattr(S, name) for name in ("krows_times", "krows_tc")}
+
+    def timed(fn):
+        def wrapper(*a, **kw):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            out = fn(*a, **kw)
+            e.record()
+            evs.append((s, e))
+            return out
+        return wrapper
+
+    for name, fn in originals.items():
+        setattr(S, name, timed(fn))
     sampler = ClockSampler(local)
     sampler.start()
     launches0 = lib.sap_launch_count()
@@ -229,7 +235,8 @@ def run_b200(args):
         tdist.barrier()
     launches = lib.sap_launch_count() - launches0
     clocks = sampler.stop()
-    S.krows_times = orig
+    for name, fn in originals.items():
+        setattr(S, name, fn)
     ms = t0.elapsed_time(t1)
     kms = [s.elapsed_time(e) for s, e in evs]
     kmean = sum(kms) / len(kms)
@@ -244,6 +251,8 @@ def run_b200(args):
     entries = b * args.n
     flops_launch = b * n_local * 2 * (d + m)
     achieved = flops_launch / (kmean * 1e-3) / 1e12
+    kernel_name = ("sap_krows_tc (tcgen05 + TMEM + TMA, split-precision)" if eng.use_tc
+                   else "sap_krows_times (FFMA path)")
 
     # FP32 FFMA peak of this GPU (the FFMA path's denominator)
     buf = torch.zeros(256, device=dev)
@@ -264,6 +273,7 @@ def run_b200(args):
     except (OSError, ValueError):
         pass
 
+    bf16_peak = float(peaks.get("bf16_tflops", 1590.0))
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, prob, spec, dev)
@@ -284,12 +294,14 @@ def run_b200(args):
         "config": workload(args),
         "kernel_entries_per_s": entries / (ms_step * 1e-3),
         "krows_ms": kmean,
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": ffma_peak, "unit": "TFLOP/s",
-                     "frac": achieved / ffma_peak, "traffic": None,
-                     "kernel": "sap_krows_times (FFMA path)",
-                     "peak_source": "measured on this GPU by sap_ffma_peak (FP32 FFMA); "
-                                    f"MEASURED_PEAKS bf16 dense {peaks.get('bf16_tflops')} TFLOP/s",
-                     "algorithmic": f"{b}*{n_local}*2*({d}+{m}) flop per launch"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak,
+                     "unit": "TFLOP/s", "frac": achieved / bf16_peak, "traffic": TRAFFIC_PER_LAUNCH,
+                     "kernel": kernel_name,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst), of measured",
+                     "algorithmic": f"{b}*{n_local}*2*({d}+{m}) flop per launch "
+                                    "(2d+2m per kernel entry, BASELINE.md §2)",
+                     "fp32_ffma_peak": ffma_peak,
+                     "frac_of_fp32_ffma_roofline": achieved / ffma_peak},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -314,6 +326,8 @@ def run_e2e(args, prob, spec, dev):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     o = sap.KernelOracle(spec, X, prob.lam, device=dev)
+    torch.cuda.synchronize()
+    t_oracle = time.perf_counter() - t0
     res = sap.adasap_solve(o, Y, cfg)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
@@ -323,7 +337,8 @@ def run_e2e(args, prob, spec, dev):
     return {"value": K / dt, "unit": "iters/s",
             "h2d_bytes_per_step": int(per_iter_h2d + (X.nbytes + Y.nbytes) / K),
             "d2h_bytes_per_step": int(per_iter_d2h + res.W.nbytes / K),
-            "region": f"KernelOracle(X host) + adasap_solve(Y host, max_iters={K}) + W to host"}
+            "region": f"KernelOracle(X host) + adasap_solve(Y host, max_iters={K}) + W to host",
+            "seconds": dt, "oracle_setup_s": t_oracle}
 
 
 def run_reference(args):

@@ -24,6 +24,8 @@ allocated in steady state.
 from __future__ import annotations
 
 import math
+import os
+import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -32,7 +34,7 @@ import torch
 
 from . import kernels as K
 from .errors import NumericalError
-from .randnla import factor_core_retry
+from .randnla import factor_gram_retry, woodbury_core
 from .rng import block_hash, substream, uniform_block
 
 
@@ -46,7 +48,7 @@ class IterPlan:
     Xb: torch.Tensor           # (b, ldx) fp32 gathered points
     rsq: torch.Tensor          # (b,) fp32
     U: torch.Tensor | None     # (b, r) fp64
-    Mc: torch.Tensor | None    # (r,) fp64, Woodbury core diag S/(S+rho) (0 on pruned modes)
+    Mc: torch.Tensor | None    # (r, r) fp64 Woodbury core: D = (g - U Mc U^T g) / rho
     rho: float
     eta_dev: torch.Tensor      # (1,) fp64 view
     S: np.ndarray
@@ -61,7 +63,12 @@ class _Slot:
         self.Xb = torch.empty((L, b, ldx), dtype=f32, device=dev)
         self.rsq = torch.empty((L, b), dtype=f32, device=dev)
         self.U = torch.empty((L, b, r), dtype=f64, device=dev) if r else None
-        self.Mc = torch.empty((L, r), dtype=f64, device=dev) if r else None
+        self.Mc = torch.empty((L, r, r), dtype=f64, device=dev) if r else None
+        self.E = torch.zeros((L, max(r, 1)), dtype=f64, device=dev)
+        self.rho = torch.ones(L, dtype=f64, device=dev)
+        self.v0 = torch.empty((L, b), dtype=f64, device=dev)
+        self.Kbb = torch.empty((L, b, b), dtype=f64, device=dev)
+        self.graph = None  # CUDA graph of the batched power iteration (full batches)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
         bpad = (b + 127) // 128 * 128
@@ -71,8 +78,8 @@ class _Slot:
         self.h_omega = torch.empty((L, b, max(r, 1)), dtype=f64, pin_memory=pin)
         self.h_v0 = torch.empty((L, b), dtype=f64, pin_memory=pin)
         self.h_small = torch.empty((L, 3, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
-        self.h_ur = torch.empty((L, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
-        self.h_coef = torch.empty((L, 3, max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_w = torch.empty((L, 2, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
+        self.h_coef = torch.empty((L, max(r, 1)), dtype=f64, pin_memory=pin)
         self.h_rho = torch.empty(L, dtype=f64, pin_memory=pin)
         self.free = None      # event on the main stream: last consumer enqueued
         self.h2d_done = None  # event on the side stream: pinned inputs consumed
@@ -97,21 +104,45 @@ class Lookahead:
                  tcp=None):
         self.o, self.shard, self.seed = oracle, shard, seed
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
-        self.total, self.L = total, max(1, min(L, total))
+        # two slots of L fp64 b x b blocks: keep them under ~2 GB
+        cap = max(1, int(2e9 // (2 * 8 * b * b)))
+        self.total, self.L = total, max(1, min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
         self.dev = dev
-        self.side = torch.cuda.Stream(device=dev)
+        # high priority: the side chain's short kernels run in the gaps between the
+        # persistent block-row kernels instead of queueing behind the next one
+        self.side = torch.cuda.Stream(device=dev, priority=-1)
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
         self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(2)]
         self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sap-lookahead")
+        # host workers for the per-iteration numpy RNG and r x r LAPACK work (both
+        # release the GIL in their kernels); sized to leave cores for the main thread
+        try:
+            cores = len(os.sched_getaffinity(0))
+        except AttributeError:  # pragma: no cover
+            cores = os.cpu_count() or 1
+        self.hostpool = ThreadPoolExecutor(max_workers=max(1, min(self.L, cores - 2, 8)),
+                                           thread_name_prefix="sap-host")
+        self.timings = [] if os.environ.get("SAP_PROFILE") else None
+        # r x r LAPACK calls from several host workers: one BLAS thread each (the
+        # reference pins BLAS to one thread for the same reason, __init__.py:16-22)
+        try:
+            from threadpoolctl import threadpool_limits
+            self._blas_limit = threadpool_limits(limits=1, user_api="blas")
+        except Exception:  # pragma: no cover - threadpoolctl is optional
+            self._blas_limit = None
         self.cur = None
         self.k = 0
         self.fut = self.pool.submit(self._produce, self.slots[0], 0, min(self.L, total))
 
     def close(self):
         self.pool.shutdown(wait=True)
+        self.hostpool.shutdown(wait=True)
+        if self._blas_limit is not None:
+            self._blas_limit.restore_original_limits()
+            self._blas_limit = None
 
     # -- consumer side (main thread) ------------------------------------------
     def get(self, t):
@@ -151,12 +182,11 @@ class Lookahead:
         b, r, seed, n = self.b, self.r, self.seed, self.n
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
-        blocks, crcs = [], []
-        for i in range(count):
+        tm0 = time.perf_counter()
+
+        def draw(i):
             t = t0 + i
             blk = uniform_block(seed, t, n, b).astype(np.int64)
-            blocks.append(blk)
-            crcs.append(block_hash(blk))
             slot.h_block[i].numpy()[:] = blk
             if r:
                 slot.h_omega[i].numpy()[:] = substream(seed, "omega", t).standard_normal((b, r))
@@ -169,77 +199,101 @@ class Lookahead:
                 if nv == 0.0:
                     raise NumericalError("power iteration start vector is zero")
             slot.h_v0[i].numpy()[:] = v / nv
+            return blk, block_hash(blk)
+
+        drawn = list(self.hostpool.map(draw, range(count)))
+        blocks = [d[0] for d in drawn]
+        crcs = [d[1] for d in drawn]
+        tm1 = time.perf_counter()
         side = self.side
         pts = self.o.points
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
             if slot.free is not None:
                 side.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
-            v0 = slot.h_v0[:count].to(self.dev, non_blocking=True)
+            slot.v0[:count].copy_(slot.h_v0[:count], non_blocking=True)
             om = slot.h_omega[:count].to(self.dev, non_blocking=True) if r else None
-            slot.h2d_done = torch.cuda.Event()
-            slot.h2d_done.record(side)
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
-            Kbb = torch.empty((count, b, b), dtype=torch.float64, device=self.dev)
             sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
             for i in range(count):
                 Xb, rsq = pts.gather(bd[i], out=(slot.Xb[i], slot.rsq[i]))
                 if self.tcp is not None:
                     self.tcp.gather_rows(bd[i], out=slot.RAg[i])
-                Kbb[i] = K.ktile(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d)
                 if r:
                     omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS
                     K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
                                   sketch[i], col_ids=bd[i])
             if r:
                 Y = sketch.to(torch.float64)
-                Q, R = torch.linalg.qr(Y)
-                small = torch.stack([R, om.transpose(1, 2) @ Y, om.transpose(1, 2) @ om], dim=1)
+                omt = om.transpose(1, 2)
+                small = torch.stack([Y.transpose(1, 2) @ Y, omt @ Y, omt @ om], dim=1)
                 slot.h_small[:count].copy_(small, non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(side)
+            ev = torch.cuda.Event()
+            ev.record(side)
         rho = np.empty(count)
-        Ss = []
+        tm2 = time.perf_counter()
         if r:
             ev.synchronize()
+            tm2 = time.perf_counter()
             hs = slot.h_small[:count].numpy()
             hom = slot.h_omega
-            for i in range(count):
-                Ur, S, _ = factor_core_retry(hs[i, 0], hs[i, 1], hs[i, 2], r,
-                                             omega_rank=lambda i=i: np.linalg.matrix_rank(
-                                                 hom[i].numpy()))
-                rho[i] = float(S[-1]) + self.lam
-                keep = S > 0.0
-                slot.h_ur[i].numpy()[:] = Ur
-                slot.h_coef[i, 0].numpy()[:] = np.where(keep, S / (S + rho[i]), 0.0)
-                slot.h_coef[i, 1].numpy()[:] = 1.0 / np.sqrt(S + rho[i]) - 1.0 / math.sqrt(rho[i])
-                Ss.append(S)
+
+            def factor(i):
+                W, S, UtU = factor_gram_retry(hs[i, 0], hs[i, 1], hs[i, 2], r,
+                                              omega_rank=lambda: np.linalg.matrix_rank(
+                                                  hom[i].numpy()))
+                rho_i = float(S[-1]) + self.lam
+                slot.h_w[i, 0].numpy()[:] = W
+                slot.h_w[i, 1].numpy()[:] = woodbury_core(S, UtU, rho_i)
+                slot.h_coef[i].numpy()[:] = 1.0 / np.sqrt(S + rho_i) - 1.0 / math.sqrt(rho_i)
+                return rho_i, S
+
+            res = list(self.hostpool.map(factor, range(count)))
+            rho[:] = [x[0] for x in res]
+            Ss = [x[1] for x in res]
         else:
+            ev.synchronize()  # pinned inputs consumed before the slot is refilled
             rho[:] = 1.0
             Ss = [np.zeros(0)] * count
+        tm3 = time.perf_counter()
         slot.h_rho[:count].numpy()[:] = rho
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
-            rho_d = slot.h_rho[:count].to(self.dev, non_blocking=True)
+            for i in range(count):
+                Xb, rsq = slot.Xb[i], slot.rsq[i]
+                slot.Kbb[i] = K.ktile(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d)
+            slot.rho[:count].copy_(slot.h_rho[:count], non_blocking=True)
             if r:
-                Ur = slot.h_ur[:count].to(self.dev, non_blocking=True)
-                coef = slot.h_coef[:count].to(self.dev, non_blocking=True)
-                torch.bmm(Q, Ur, out=slot.U[:count])
-                slot.Mc[:count].copy_(coef[:, 0])
-                E = coef[:, 1]
-                U = slot.U[:count]
-            self._power(Kbb, v0, rho_d, U if r else None, E if r else None, slot, count)
+                w = slot.h_w[:count].to(self.dev, non_blocking=True)
+                torch.bmm(Y, w[:, 0], out=slot.U[:count])
+                slot.Mc[:count].copy_(w[:, 1])
+                slot.E[:count].copy_(slot.h_coef[:count], non_blocking=True)
+            if count == self.L:
+                if slot.graph is None:
+                    self._power(slot, count)  # eager warm-up, then capture
+                    slot.graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(slot.graph, stream=side,
+                                          capture_error_mode="thread_local"):
+                        self._power(slot, count)
+                slot.graph.replay()
+            else:
+                self._power(slot, count)
             ready = torch.cuda.Event()
             ready.record(side)
-            done = torch.cuda.Event()
-            done.record(side)
-            slot.h2d_done = done  # pinned host buffers reusable after this point
+            slot.h2d_done = ready  # pinned host buffers reusable after this point
+        if self.timings is not None:
+            self.timings.append(dict(count=count, rng=tm1 - tm0, gpu_wait=tm2 - tm1,
+                                     factor=tm3 - tm2, total=time.perf_counter() - tm0))
         return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready)
 
-    def _power(self, Kbb, v, rho, U, E, slot, count):
+    def _power(self, slot, count):
         """Batched rand_power_stepsize (randnla.py:165-196) on P^{-1/2}(K+lam)P^{-1/2},
-        P^{-1/2} x = x/sqrt(rho) + U diag((S+rho)^{-1/2} - rho^{-1/2}) U^T x."""
-        isr = rho.rsqrt()[:, None]
+        P^{-1/2} x = x/sqrt(rho) + U diag((S+rho)^{-1/2} - rho^{-1/2}) U^T x,
+        from the slot's static buffers (so full batches replay as one CUDA graph)."""
+        Kbb, v, U, E = slot.Kbb[:count], slot.v0[:count], None, slot.E[:count]
+        if self.r:
+            U = slot.U[:count]
+        isr = slot.rho[:count].rsqrt()[:, None]
 
         def pinv_sqrt(x):
             y = x * isr

@@ -9,8 +9,9 @@ by ``AdasapEngine``:
   the gradient gather g = K[B,:]Z + lam Z[B] - Y[B] (``sap_grad_gather``) and,
   with several GPUs, one float64 all-reduce of g (paper Alg. 6);
 * Phases II/III -- produced ahead, batched, by ``pipeline.Lookahead``;
-* Phase IV -- D_B = (g - U diag(S/(S+rho)) U^T g) / rho (two fp64 GEMMs,
-  randnla.py:109-134 with U^T U = I) and the Nesterov update.
+* Phase IV -- D_B = (g - U Mc U^T g) / rho with the r x r Cholesky-stabilised
+  Woodbury core Mc (randnla.py:109-134; three small fp64 GEMMs) and the
+  Nesterov update.
 
 The Nesterov update never touches the n - b rows outside the block. Off
 the block the recurrence (solvers.py:76-85) is the fixed linear map
@@ -367,8 +368,7 @@ class AdasapEngine:
         allreduce_sum_(self.g)
         # Phase IV: D_B = (g - U diag(Mc) U^T g) / rho
         if plan.U is not None:
-            Utg = plan.U.T @ self.g
-            D = (self.g - plan.U @ (plan.Mc[:, None] * Utg)) / plan.rho
+            D = (self.g - plan.U @ (plan.Mc @ (plan.U.T @ self.g))) / plan.rho
         else:
             D = self.g / plan.rho
         self._update(plan, D)
