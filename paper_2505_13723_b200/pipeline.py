@@ -135,6 +135,19 @@ class Lookahead:
             self._blas_limit = None
         self.cur = None
         self.k = 0
+        # capture both slots' power-iteration graphs up front (static buffers; the
+        # values are filled per batch), so no capture lands inside a timed solve
+        if self.L > 1:
+            with torch.cuda.device(dev), torch.cuda.stream(self.side):
+                for slot in self.slots:
+                    slot.v0.fill_(1.0)
+                    slot.Kbb.zero_()
+                    self._power(slot, self.L)  # warm-up (allocator, cuBLAS handles)
+                    slot.graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(slot.graph, stream=self.side,
+                                          capture_error_mode="thread_local"):
+                        self._power(slot, self.L)
+                    slot.bad.zero_()
         self.fut = self.pool.submit(self._produce, self.slots[0], 0, min(self.L, total))
 
     def close(self):
@@ -268,13 +281,7 @@ class Lookahead:
                 torch.bmm(Y, w[:, 0], out=slot.U[:count])
                 slot.Mc[:count].copy_(w[:, 1])
                 slot.E[:count].copy_(slot.h_coef[:count], non_blocking=True)
-            if count == self.L:
-                if slot.graph is None:
-                    self._power(slot, count)  # eager warm-up, then capture
-                    slot.graph = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(slot.graph, stream=side,
-                                          capture_error_mode="thread_local"):
-                        self._power(slot, count)
+            if count == self.L and slot.graph is not None:
                 slot.graph.replay()
             else:
                 self._power(slot, count)

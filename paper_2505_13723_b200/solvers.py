@@ -468,10 +468,9 @@ class AdasapEngine:
         if sh.size == 0:
             part = torch.zeros(1, dtype=torch.float64, device=self.dev)
         else:
+            # rows of this shard against all points: the same fused product (K5)
             ids = torch.arange(sh.lo, sh.hi, device=self.dev, dtype=torch.int64)
-            Rs, rsq = self.o.points.Xs[sh.lo:sh.hi], self.o.points.sqn[sh.lo:sh.hi]
-            KW = torch.empty((sh.size, self.m), dtype=torch.float32, device=self.dev)
-            krows_times(self.o.spec, self.o.points, Rs, rsq, ids, Wcm, KW)
+            KW = self.o.rows_times_device(ids, Wcm)
             res = KW.double() + self.lam * W_local.double() - self.Y[:, :sh.size].T.double()
             part = (res * res).sum().reshape(1)
         allreduce_sum_(part)
