@@ -40,8 +40,8 @@ for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
     os.environ.setdefault(_v, "1")
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at this
-# config, from the committed ncu capture (profiles/); None until captured.
-TRAFFIC_PER_LAUNCH = None
+# config, from the committed ncu capture (profiles/); re-capture when the kernel changes.
+TRAFFIC_PER_LAUNCH = 505_737_728  # profiles/r01_krows_tc_m32_ncu_summary.txt (486.38 MB read + 19.36 MB write)
 
 CONFIG = dict(n=1_000_000, d=9, family="matern32", b=2000, m=65, r=100, lam=1e-2, seed=0)
 METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target RMSE"

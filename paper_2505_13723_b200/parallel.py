@@ -76,6 +76,21 @@ def allreduce_sum_(t):
     return t
 
 
+def gather_rows(local, n, shard):
+    """Concatenate the row shards of an (n_local x m) tensor on every rank
+    (the inverse of ShardInfo.of); works for CUDA (NCCL) and CPU (gloo)."""
+    if shard.world == 1:
+        return local
+    sizes = [hi - lo for lo, hi in partition(n, shard.world)] if n >= shard.world else \
+        [n if r == 0 else 0 for r in range(shard.world)]
+    mx = max(sizes)
+    buf = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    buf[:local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in sizes]
+    tdist.all_gather(parts, buf)
+    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+
+
 def init_from_env(backend=None):
     """Initialise torch.distributed from torchrun's environment, if present."""
     if "RANK" not in os.environ or "WORLD_SIZE" not in os.environ:

@@ -44,7 +44,7 @@ from . import _native as nat
 from .dist import WorkerPool
 from .errors import ConfigError, ContractError
 from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
-from .parallel import ShardInfo, allreduce_sum_, current_shard
+from .parallel import ShardInfo, allreduce_sum_, current_shard, gather_rows
 from .pipeline import Lookahead
 from .rng import block_hash
 
@@ -447,17 +447,7 @@ class AdasapEngine:
 
     def gather_full(self, local):
         """Concatenate shards (n x m) on every rank."""
-        if self.shard.world == 1:
-            return local
-        import torch.distributed as tdist
-        from .dist import partition
-        sizes = [hi - lo for lo, hi in partition(self.n, self.shard.world)]
-        mx = max(sizes)
-        buf = torch.zeros((mx, self.m), dtype=local.dtype, device=local.device)
-        buf[:local.shape[0]] = local
-        parts = [torch.empty_like(buf) for _ in sizes]
-        tdist.all_gather(parts, buf)
-        return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+        return gather_rows(local, self.n, self.shard)
 
     def relative_residual(self, W_local, ynorm):
         """||K W + lam W - Y||_F / ||Y||_F over this shard's rows, summed over ranks
