@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "krows_tc.cuh"
+#include "krows_tc2.cuh"
 
 namespace sap {
 
@@ -24,6 +25,12 @@ bool launch_tc_m32(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &
                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
 bool launch_tc_m52(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
+bool launch_tc2_rbf(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
+                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
+bool launch_tc2_m32(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
+                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
+bool launch_tc2_m52(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
+                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // augmented features for the 3-term tf32 distance GEMM
@@ -238,9 +245,32 @@ int sap_tc_supported(int d, int m) {
   return (3 * d + 4 <= 64 && tc_fits(nz, ka)) ? 1 : 0;
 }
 
+// splits for the CTA-pair kernel: whole waves of 74 pairs over 256-row tiles
+int tc2_splits(int64_t b, int64_t tiles) {
+  const int64_t rt = (b + 2 * BM - 1) / (2 * BM);
+  const int64_t pairs = kSms / 2;
+  int64_t best = 1;
+  double best_eff = -1.0;
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(tiles / 4, 4096));
+  for (int64_t s = 1; s <= std::min<int64_t>(max_s, 8 * pairs); ++s) {
+    const int64_t total = rt * s;
+    const int64_t waves = (total + pairs - 1) / pairs;
+    if (waves > 8) break;
+    const double eff = double(total) / double(waves * pairs);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return int(best);
+}
+
+bool use_pair(int nz, int ka) {
+  const char *e = getenv("SAP_TC_PAIR");
+  return (!e || atoi(e) != 0) && tck2::tc2_fits(nz, ka);
+}
+
 size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols) {
-  const int64_t tiles = (ncols + NT - 1) / NT;
-  return size_t(tc_splits(b, tiles)) * size_t(b) * size_t(m) * sizeof(float);
+  const int64_t t1 = (ncols + NT - 1) / NT, t2 = (ncols + tck2::NT - 1) / tck2::NT;
+  const int64_t s = std::max<int64_t>(tc_splits(b, t1), tc2_splits(b, t2));
+  return size_t(s) * size_t(b) * size_t(m) * sizeof(float);
 }
 
 int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64_t bpad,
@@ -249,54 +279,85 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,
                  size_t ws_bytes, void *stream) {
   if (b <= 0 || m <= 0 || ncols <= 0 || (ka != 32 && ka != 64) || nz % 16 || nz < m ||
-      nz > 128 || bpad % BM || bpad < b || ldz % 8 || ldz < ncols)
+      nz > 128 || bpad % BM || bpad < b || ldz % 8 || ldz < ncols || ncols > INT32_MAX)
     return fail(SAP_ERR_CONTRACT, "krows_tc: bad shape b=%lld m=%d nz=%d ncols=%lld ka=%d",
                 (long long)b, m, nz, (long long)ncols, ka);
   if (ldo < m) return fail(SAP_ERR_CONTRACT, "krows_tc: ldo < m");
-  const int64_t tiles = (ncols + NT - 1) / NT;
+  const bool pair = use_pair(nz, ka) && bpad % (2 * BM) == 0;
+  const int nt = pair ? tck2::NT : NT;
+  const int64_t tiles = (ncols + nt - 1) / nt;
   Params p{};
   p.b = b;
   p.ncols = ncols;
   p.col_base = col_base;
   p.row_ids = row_ids;
   p.m = m;
-  p.row_tiles = int(bpad / BM);
+  p.row_tiles = int(bpad / (pair ? 2 * BM : BM));
   p.tiles = tiles;
-  p.splits = tc_splits(b, tiles);
+  p.splits = pair ? tc2_splits(b, tiles) : tc_splits(b, tiles);
   {
     const char *dbg = getenv("SAP_TC_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
+  }
+  static unsigned long long *prof_buf = nullptr;
+  if (p.debug == 9) {
+    if (!prof_buf) cudaMalloc(&prof_buf, 148 * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof_buf, 0, 148 * 16 * sizeof(unsigned long long), (cudaStream_t)stream);
+    p.prof = prof_buf;
   }
   const size_t need = size_t(p.splits) * size_t(b) * size_t(m) * sizeof(float);
   if (!ws || ws_bytes < need)
     return fail(SAP_ERR_CONTRACT, "krows_tc: workspace %zu < %zu bytes", ws_bytes, need);
   p.part = static_cast<float *>(ws);
-  if (!tc_fits(nz, ka))
+  if (!pair && !tc_fits(nz, ka))
     return fail(SAP_ERR_CONTRACT, "krows_tc: nz=%d ka=%d tile ring does not fit shared memory", nz,
                 ka);
 
+  // B operands: the pair kernel stages half a column tile (64 points) and
+  // half of the right-hand sides (nz/2) per CTA
+  const uint32_t xbox = pair ? tck2::NT / 2 : NT;
+  const uint32_t zbox = pair ? nz / 2 : nz;
   CUtensorMap tm_rows, tm_cols, tm_zhi, tm_zlo;
   if (!make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RAg, ka, bpad, size_t(ka) * 4, 32, BM) ||
-      !make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CA, ka, ncols, size_t(ka) * 4, 32, NT) ||
-      !make_map(&tm_zhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zhi, ncols, nz, size_t(ldz) * 2, 64, nz) ||
-      !make_map(&tm_zlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zlo, ncols, nz, size_t(ldz) * 2, 64, nz))
+      !make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CA, ka, ncols, size_t(ka) * 4, 32, xbox) ||
+      !make_map(&tm_zhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zhi, ncols, nz, size_t(ldz) * 2, 64, zbox) ||
+      !make_map(&tm_zlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zlo, ncols, nz, size_t(ldz) * 2, 64, zbox))
     return fail(SAP_ERR_DEVICE, "krows_tc: cuTensorMapEncodeTiled failed");
 
   cudaStream_t st = (cudaStream_t)stream;
   const int units = p.row_tiles * p.splits;
-  const int grid = std::min(units, kSms);
+  const int grid = pair ? 2 * std::min(units, kSms / 2) : std::min(units, kSms);
   int rc;
   bool launched;
   if (family == SAP_RBF)
-    launched = launch_tc_rbf(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
+    launched = pair ? launch_tc2_rbf(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st)
+                    : launch_tc_rbf(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
   else if (family == SAP_MATERN32)
-    launched = launch_tc_m32(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
+    launched = pair ? launch_tc2_m32(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st)
+                    : launch_tc_m32(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
   else if (family == SAP_MATERN52)
-    launched = launch_tc_m52(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
+    launched = pair ? launch_tc2_m52(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st)
+                    : launch_tc_m52(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
   else
     return fail(SAP_ERR_CONTRACT, "krows_tc: unknown family %d", family);
   if (!launched) return fail(SAP_ERR_CONTRACT, "krows_tc: shape nz=%d ka=%d unsupported", nz, ka);
-  if ((rc = check_launch("krows_tc_kernel")) != SAP_OK) return rc;
+  if ((rc = check_launch(pair ? "krows_tc2_kernel" : "krows_tc_kernel")) != SAP_OK) return rc;
+  if (p.prof) {  // profiling only: per-role cycle totals, averaged over CTAs
+    unsigned long long h[148 * 16];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost);
+    const char *names[12] = {"prod.wait_empty", "prod.issue", "mma.wait_full", "mma.wait_pfull",
+                             "mma.wait_gempty", "mma.issue_g1", "mma.issue_g2", "epi.wait_sfull",
+                             "epi.convert", "epi.arrive", "epi.drain", "kernel"};
+    for (int k = 0; k < 12; ++k) {
+      double s0 = 0, s1 = 0; int n0 = 0, n1 = 0;
+      for (int g = 0; g < grid; ++g) {
+        if (g % 2 == 0) { s0 += h[g * 16 + k]; ++n0; } else { s1 += h[g * 16 + k]; ++n1; }
+      }
+      fprintf(stderr, "[tc prof] %-18s leader %12.0f  peer %12.0f cycles/CTA\n", names[k],
+              n0 ? s0 / n0 : 0.0, n1 ? s1 / n1 : 0.0);
+    }
+  }
   const int64_t tot = b * m;
   tc_reduce_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(p.part, p.splits, b, m,
                                                                 float(variance), zscale, out, ldo,

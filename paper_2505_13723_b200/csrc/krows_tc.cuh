@@ -63,6 +63,7 @@ struct Params {
   int64_t tiles;           // column tiles of NT points
   float *part;             // [splits][b][m] partial sums (scaled)
   int debug;               // profiling switches, 0 in production
+  unsigned long long *prof;  // per-CTA role timers (SAP_TC_DEBUG=9), else NULL
 };
 
 template <int NZ, int KA>
@@ -87,12 +88,14 @@ __device__ __forceinline__ void split_range(int64_t tiles, int splits, int s, in
 
 template <int FAM>
 __device__ __forceinline__ float pvalue(float s) {
-  s = fmaxf(s, 0.0f);
   if constexpr (FAM == SAP_RBF) {
-    return ex2_approx(14.0f - s);
+    return ex2_approx(14.0f - fmaxf(s, 0.0f));
   } else {
-    // the 2^14 scale rides on the polynomial, so ex2 takes -t directly
-    const float t = sqrt_approx(s);
+    // the 2^14 scale rides on the polynomial, so ex2 takes -t directly;
+    // t = s * rsqrt(s) (MUFU.RSQ, faster than MUFU.SQRT here) with s floored at
+    // 1e-30, which also clamps negative rounding, so s <= 0 gives t ~ 0
+    s = fmaxf(s, 1e-30f);
+    const float t = s * rsqrt_approx(s);
     const float e = ex2_approx(-t);
     if constexpr (FAM == SAP_MATERN32) {
       return fmaf(t, kPScale * kLn2, kPScale) * e;

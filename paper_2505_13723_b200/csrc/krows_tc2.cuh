@@ -1,0 +1,450 @@
+// CTA-pair (cta_group::2) version of the tensor-core block-row product.
+//
+// Same math as krows_tc.cuh (GEMM1 tf32 3-term distances -> TMEM, epilogue
+// P = 2^14 k(S) split fp16 hi/lo -> TMEM, GEMM2 f16 with A from TMEM), but
+// every MMA spans the two SMs of a cluster pair: M = 256 block rows (128 per
+// CTA's TMEM) and each CTA stages only HALF of the B operands (its 64 of the
+// 128 points of a column tile for GEMM1, its nz/2 of the right-hand sides for
+// GEMM2). Per SM this halves the shared-memory footprint and L2->SM traffic
+// of the column tiles and halves the MMA instructions and barrier round trips
+// the single issuing thread spends per kernel entry -- the per-tile
+// synchronisation of the single-thread roles is what bounded the 1-CTA kernel
+// (profiles/).
+//
+// Barrier ownership: full/p_full/g_empty/a_full live in the leader CTA (rank
+// 0) and receive the peer's TMA bytes (peer bit cleared, cta_group::2 TMA)
+// and remote epilogue arrivals (mapa + release.cluster); s_full/empty/
+// a_empty/g_full are signalled in both CTAs by multicast tcgen05.commit.
+#pragma once
+
+#include "krows_tc.cuh"
+
+namespace sap {
+namespace tck2 {
+
+using tck::BM;
+using tck::kPScale;
+using tck::kSmemCap;
+using tck::Params;
+using tck::pvalue;
+using tck::split2;
+using tck::split_range;
+using tck::kDescBase;
+
+constexpr int NT = 128;     // points per column tile (64 staged per CTA)
+constexpr int NB = 2;       // S/P tiles in flight in TMEM
+constexpr int kSeg = 8;     // tiles per TMEM accumulator segment
+constexpr int kThreads = 384;
+
+template <int NZ, int KA>
+struct Geometry2 {
+  static constexpr uint32_t a_bytes = BM * KA * 4;             // this CTA's 128 block rows
+  static constexpr uint32_t x_bytes = (NT / 2) * KA * 4;       // this CTA's 64 points
+  static constexpr uint32_t z_atom = (NZ / 2) * 128;           // 64 points x nz/2 columns
+  static constexpr uint32_t z_bytes = 2 * z_atom;              // 128 points
+  static constexpr uint32_t stage_bytes = x_bytes + 2 * z_bytes;
+  static constexpr uint32_t fixed = 1024 + 2 * a_bytes + 512;
+  static constexpr uint32_t stages_raw = (kSmemCap - fixed) / stage_bytes;
+  static constexpr uint32_t STAGES = stages_raw > 8 ? 8 : stages_raw;
+  static constexpr uint32_t smem = fixed + STAGES * stage_bytes;
+  static constexpr bool fits = STAGES >= 3 && NZ % 32 == 0 && NZ >= 32 && NZ <= 128;
+};
+
+template <int FAM, int NZ, int KA>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    krows_tc2_kernel(const __grid_constant__ CUtensorMap tm_rows,
+                     const __grid_constant__ CUtensorMap tm_cols,
+                     const __grid_constant__ CUtensorMap tm_zhi,
+                     const __grid_constant__ CUtensorMap tm_zlo, const Params p) {
+  using Geo = Geometry2<NZ, KA>;
+  constexpr uint32_t STAGES = Geo::STAGES;
+  constexpr int KATOMS = KA / 32;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t cr = tc::cluster_ctarank();   // 0 = leader (issues the MMAs)
+  const unsigned long long kstart = clock64();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  uint8_t *sA = smem;                          // [2][a_bytes]
+  uint8_t *sStage = smem + 2 * Geo::a_bytes;   // [STAGES][stage_bytes]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sStage + STAGES * Geo::stage_bytes);
+  uint64_t *full = bars;                  // [STAGES]  leader: TMA bytes of both CTAs
+  uint64_t *empty = full + STAGES;        // [STAGES]  both: multicast commit
+  uint64_t *a_full = empty + STAGES;      // [2]       leader
+  uint64_t *a_empty = a_full + 2;         // [2]       both
+  uint64_t *s_full = a_empty + 2;         // [NB]      both
+  uint64_t *p_full = s_full + NB;         // [NB]      leader: 16 warp arrivals
+  uint64_t *g_full = p_full + NB;         // [2]       both
+  uint64_t *g_empty = g_full + 2;         // [2]       leader: 16 warp arrivals
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(g_empty + 2);
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < STAGES; ++s) {
+      tc::mbar_init(tc::smem_u32(&full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&empty[s]), 1);
+    }
+    for (int k = 0; k < NB; ++k) {
+      tc::mbar_init(tc::smem_u32(&s_full[k]), 1);
+      tc::mbar_init(tc::smem_u32(&p_full[k]), 16);
+    }
+    for (int k = 0; k < 2; ++k) {
+      tc::mbar_init(tc::smem_u32(&a_full[k]), 1);
+      tc::mbar_init(tc::smem_u32(&a_empty[k]), 1);
+      tc::mbar_init(tc::smem_u32(&g_full[k]), 1);
+      tc::mbar_init(tc::smem_u32(&g_empty[k]), 16);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tm_rows);
+    tc::prefetch_tmap(&tm_cols);
+    tc::prefetch_tmap(&tm_zhi);
+    tc::prefetch_tmap(&tm_zlo);
+  }
+  if (warp == 2) {
+    tc::tmem_alloc_pair(tc::smem_u32(tmem_slot), 512);
+    tc::tmem_relinquish_pair();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // barriers of both CTAs initialised before any remote signal
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int units = p.row_tiles * p.splits;  // row_tiles counts 256-row pair tiles here
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (tc::elect_one()) {
+      uint32_t s = 0, ph = 0;
+      int uc = 0;
+      const uint32_t full0 = tc::smem_u32(full), empty0 = tc::smem_u32(empty);
+      const uint32_t stage0 = tc::smem_u32(sStage);
+      unsigned long long tw = 0, ti = 0, c0;
+      for (int u = pair; u < units; u += npairs, ++uc) {
+        const int rt = u % p.row_tiles, split = u / p.row_tiles;
+        int64_t t0, t1;
+        split_range(p.tiles, p.splits, split, t0, t1);
+        const int ab = uc & 1;
+        tc::mbar_wait(tc::smem_u32(&a_empty[ab]), ((uc >> 1) & 1) ^ 1);
+        const uint32_t abar = tc::smem_u32(&a_full[ab]);
+        if (cr == 0) tc::mbar_expect_tx(abar, 2 * Geo::a_bytes);
+#pragma unroll
+        for (int ka = 0; ka < KATOMS; ++ka)
+          tc::tma_load_2d_pair(tc::smem_u32(sA + ab * Geo::a_bytes + ka * BM * 128), &tm_rows,
+                               abar, ka * 32, rt * 2 * BM + int(cr) * BM);
+        for (int64_t t = t0; t < t1; ++t) {
+          c0 = clock64();
+          tc::mbar_wait(empty0 + 8 * s, ph ^ 1);
+          const unsigned long long c1 = clock64();
+          tw += c1 - c0;
+          const uint32_t fbar = full0 + 8 * s;
+          if (cr == 0) tc::mbar_expect_tx(fbar, 2 * Geo::stage_bytes);
+          const uint32_t st = stage0 + s * Geo::stage_bytes;
+          const int32_t col0 = int32_t(t * NT);
+#pragma unroll
+          for (int ka = 0; ka < KATOMS; ++ka)
+            tc::tma_load_2d_pair(st + ka * (NT / 2) * 128, &tm_cols, fbar, ka * 32,
+                                 col0 + int(cr) * (NT / 2));
+#pragma unroll
+          for (int za = 0; za < 2; ++za) {
+            tc::tma_load_2d_pair(st + Geo::x_bytes + za * Geo::z_atom, &tm_zhi, fbar,
+                                 col0 + za * 64, int(cr) * (NZ / 2));
+            tc::tma_load_2d_pair(st + Geo::x_bytes + Geo::z_bytes + za * Geo::z_atom, &tm_zlo,
+                                 fbar, col0 + za * 64, int(cr) * (NZ / 2));
+          }
+          ti += clock64() - c1;
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+      if (p.prof) {
+        p.prof[blockIdx.x * 16 + 0] = tw;
+        p.prof[blockIdx.x * 16 + 1] = ti;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (cr == 0 && tc::elect_one()) {
+      constexpr uint32_t id1 = tc::idesc(2, 2 * BM, NT);  // tf32, M=256, N=128
+      constexpr uint32_t id2 = tc::idesc(0, 2 * BM, NZ);  // f16,  M=256, N=nz
+      const uint32_t full0 = tc::smem_u32(full), empty0 = tc::smem_u32(empty);
+      const uint32_t sfull0 = tc::smem_u32(s_full), pfull0 = tc::smem_u32(p_full);
+      const uint64_t stage_desc0 = kDescBase | (tc::smem_u32(sStage) >> 4);
+      const uint64_t a_desc0 = kDescBase | (tc::smem_u32(sA) >> 4);
+      uint32_t s1 = 0, ph1 = 0, r1 = 0;    // GEMM1 cursor (one tile ahead)
+      uint32_t s2 = 0, r2 = 0, ph2 = 0;    // GEMM2 cursor
+      uint32_t sc = 0;
+      int uc = 0;
+      unsigned long long wf = 0, wp = 0, wg = 0, i1 = 0, i2 = 0, cc;
+      for (int u = pair; u < units; u += npairs, ++uc) {
+        const int split = u / p.row_tiles;
+        int64_t t0, t1;
+        split_range(p.tiles, p.splits, split, t0, t1);
+        const int nt = int(t1 - t0);
+        const int ab = uc & 1;
+        tc::mbar_wait(tc::smem_u32(&a_full[ab]), (uc >> 1) & 1);
+        tc::fence_after();
+        const uint64_t a_desc = a_desc0 + ((ab * Geo::a_bytes) >> 4);
+        auto gemm1 = [&]() {
+          cc = clock64();
+          tc::mbar_wait(full0 + 8 * s1, ph1);
+          tc::fence_after();
+          const unsigned long long cw = clock64();
+          wf += cw - cc;
+          const uint64_t x_desc = stage_desc0 + ((s1 * Geo::stage_bytes) >> 4);
+          const uint32_t d = tmem + r1 * NT;
+#pragma unroll
+          for (int k = 0; k < KA / 8; ++k) {
+            const uint32_t ko = ((k >> 2) * (BM * 128) + (k & 3) * 32) >> 4;
+            const uint32_t kx = ((k >> 2) * ((NT / 2) * 128) + (k & 3) * 32) >> 4;
+            tc::mma_tf32_ss_pair(d, a_desc + ko, x_desc + kx, id1, k > 0);
+          }
+          tc::commit_pair(sfull0 + 8 * r1);
+          i1 += clock64() - cw;
+          if (++s1 == STAGES) { s1 = 0; ph1 ^= 1; }
+          r1 = (r1 + 1) & (NB - 1);
+        };
+        if (nt > 0) gemm1();
+        if (nt == 1) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
+        uint32_t g_tmem = 0;
+        int seg_j = 0;
+        for (int j = 0; j < nt; ++j) {
+          // GEMM1 of the next tile goes first: it overwrites the S/P buffer of
+          // tile j-1, whose GEMM2 was issued earlier (in-order tensor pipe), and
+          // runs while the epilogue converts tile j
+          if (j + 1 < nt) {
+            gemm1();
+            if (j + 2 == nt) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
+          }
+          const bool seg_first = seg_j == 0;
+          const bool seg_last = seg_j == kSeg - 1 || j + 1 == nt;
+          cc = clock64();
+          if (seg_first) {
+            const int gb = sc & 1;
+            tc::mbar_wait_cluster(tc::smem_u32(&g_empty[gb]), ((sc >> 1) & 1) ^ 1);
+            g_tmem = tmem + 256 + gb * NZ;
+          }
+          const unsigned long long cg = clock64();
+          wg += cg - cc;
+          tc::mbar_wait_cluster(pfull0 + 8 * r2, ph2);
+          tc::fence_after();
+          const unsigned long long cp = clock64();
+          wp += cp - cg;
+          const uint64_t zhi = stage_desc0 + ((s2 * Geo::stage_bytes + Geo::x_bytes) >> 4);
+          const uint64_t zlo = zhi + (Geo::z_bytes >> 4);
+          const uint32_t pbase = tmem + r2 * NT;
+          if (p.debug < 4) {
+#pragma unroll
+            for (int kk = 0; kk < NT / 16; ++kk) {  // 16 points per MMA K step
+              const uint32_t bo = ((kk >> 2) * Geo::z_atom + (kk & 3) * 32) >> 4;
+              const uint32_t ahi = pbase + (kk >> 1) * 32 + (kk & 1) * 8;
+              const uint32_t acc0 = (!seg_first || kk > 0) ? 1u : 0u;
+              tc::mma_f16_ts_pair(g_tmem, ahi, zhi + bo, id2, acc0);
+              tc::mma_f16_ts_pair(g_tmem, ahi, zlo + bo, id2, 1u);
+              tc::mma_f16_ts_pair(g_tmem, ahi + 16, zhi + bo, id2, 1u);
+            }
+          }
+          tc::commit_pair(empty0 + 8 * s2);
+          if (seg_last) {
+            tc::commit_pair(tc::smem_u32(&g_full[sc & 1]));
+            ++sc;
+            seg_j = 0;
+          } else {
+            ++seg_j;
+          }
+          i2 += clock64() - cp;
+          if (++s2 == STAGES) s2 = 0;
+          r2 = (r2 + 1) & (NB - 1);
+          if (r2 == 0) ph2 ^= 1;
+        }
+      }
+      if (p.prof) {
+        p.prof[blockIdx.x * 16 + 2] = wf;
+        p.prof[blockIdx.x * 16 + 3] = wp;
+        p.prof[blockIdx.x * 16 + 4] = wg;
+        p.prof[blockIdx.x * 16 + 5] = i1;
+        p.prof[blockIdx.x * 16 + 6] = i2;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (both CTAs) =====================
+    // Both warpgroups work on every tile: warpgroup h converts S columns
+    // [64h, 64h+64) and drains accumulator columns [h*nz/2, (h+1)*nz/2).
+    // (A ping-pong split -- each warpgroup owning alternate tiles -- measured
+    // 15% slower: with a 2-deep S ring it loses GEMM1's one-tile lookahead.)
+    const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t lane_off = uint32_t(q * 32) << 16;
+    constexpr int NACC = NZ / 2;            // accumulator columns per warpgroup
+    const int g0 = h * NACC;
+    const uint32_t sfull0 = tc::smem_u32(s_full);
+    const uint32_t pfull_leader = tc::mapa(tc::smem_u32(p_full), 0);
+    const uint32_t gempty_leader = tc::mapa(tc::smem_u32(g_empty), 0);
+    uint32_t r = 0, ph = 0, sc = 0;
+    float acc[NACC];
+#pragma unroll
+    for (int c = 0; c < NACC; ++c) acc[c] = 0.0f;
+    bool pend = false, pend_last = false, pend_live = false;
+    float *pend_dst = nullptr;
+    unsigned long long es = 0, ec = 0, ed = 0, ea = 0, ce;
+    auto drain = [&]() {  // add a finished TMEM segment, one tile late
+      const int gb = sc & 1;
+      tc::mbar_wait(tc::smem_u32(&g_full[gb]), (sc >> 1) & 1);
+      tc::fence_after();
+      const uint32_t gbase = tmem + lane_off + 256 + gb * NZ + g0;
+#pragma unroll
+      for (int c0 = 0; c0 < NACC; c0 += 16) {
+        uint32_t v[16];
+        tc::ld16(gbase + c0, v);
+        tc::wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(gempty_leader + 8 * gb);
+      ++sc;
+      pend = false;
+      if (pend_last) {
+        if (pend_live) {
+#pragma unroll
+          for (int c = 0; c < NACC; ++c)
+            if (g0 + c < p.m) pend_dst[g0 + c] = acc[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NACC; ++c) acc[c] = 0.0f;
+      }
+    };
+    for (int u = pair; u < units; u += npairs) {
+      const int rt = u % p.row_tiles, split = u / p.row_tiles;
+      int64_t t0, t1;
+      split_range(p.tiles, p.splits, split, t0, t1);
+      const int64_t grow = int64_t(rt) * 2 * BM + int64_t(cr) * BM + row_in_tile;
+      const bool live = grow < p.b;
+      float *dst = p.part + (int64_t(split) * p.b + (live ? grow : 0)) * p.m;
+      const int64_t rid = (p.row_ids && live) ? p.row_ids[grow] : INT64_MIN;
+      if (t1 == t0 && live)
+        for (int c = g0; c < g0 + NACC && c < p.m; ++c) dst[c] = 0.0f;
+      int seg_j = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        ce = clock64();
+        tc::mbar_wait(sfull0 + 8 * r, ph);
+        tc::fence_after();
+        const unsigned long long cs = clock64();
+        es += cs - ce;
+        // both 32-column chunks of this warpgroup are loaded before any math, so
+        // the second load's latency hides under the first chunk's MUFU work
+        const uint32_t tbase = tmem + lane_off + r * NT + h * 64;
+        uint32_t va[32], vb[32];
+        tc::ld32(tbase, va);
+        tc::ld32(tbase + 32, vb);
+        tc::wait_ld();
+        const int64_t dc64 = rid - (p.col_base + t * NT) - h * 64;
+        const bool diag = dc64 >= 0 && dc64 < 64;
+        const int dc = int(dc64);
+        auto convert = [&](const uint32_t (&v)[32], int off, uint32_t taddr) {
+          uint32_t o[32];  // P_hi (16 packed words) then P_lo over the 32 columns
+          if (p.debug == 1 || p.debug == 4) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = v[e];
+          } else if (__any_sync(0xffffffffu, diag)) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float p0 = pvalue<FAM>(__uint_as_float(v[e]));
+              float p1 = pvalue<FAM>(__uint_as_float(v[e + 1]));
+              if (diag && dc == off + e) p0 = kPScale;
+              if (diag && dc == off + e + 1) p1 = kPScale;
+              split2(p0, p1, o[e / 2], o[16 + e / 2]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2)
+              split2(pvalue<FAM>(__uint_as_float(v[e])), pvalue<FAM>(__uint_as_float(v[e + 1])),
+                     o[e / 2], o[16 + e / 2]);
+          }
+          tc::st32(taddr, o);
+        };
+        convert(va, 0, tbase);
+        convert(vb, 32, tbase + 32);
+        tc::wait_st();
+        tc::fence_before();
+        __syncwarp();
+        const unsigned long long cw2 = clock64();
+        ec += cw2 - cs;
+        if (lane == 0) tc::mbar_arrive_cluster(pfull_leader + 8 * r);
+        r = (r + 1) & (NB - 1);
+        if (r == 0) ph ^= 1;
+        const unsigned long long ca = clock64();
+        ea += ca - cw2;
+        if (pend) drain();
+        ed += clock64() - ca;
+        if (seg_j == kSeg - 1 || t + 1 == t1) {
+          pend = true;
+          pend_last = t + 1 == t1;
+          pend_live = live;
+          pend_dst = dst;
+          seg_j = 0;
+        } else {
+          ++seg_j;
+        }
+      }
+    }
+    if (pend) drain();
+    if (p.prof && warp == 4 && lane == 0) {
+      p.prof[blockIdx.x * 16 + 7] = es;
+      p.prof[blockIdx.x * 16 + 8] = ec;
+      p.prof[blockIdx.x * 16 + 9] = ea;
+      p.prof[blockIdx.x * 16 + 10] = ed;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer's TMEM/barriers stay live until both CTAs are done
+  tc::fence_after();
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * 16 + 11] = clock64() - kstart;
+  if (warp == 2) tc::tmem_dealloc_pair(tmem, 512);
+}
+
+template <int FAM, int NZ, int KA>
+bool launch_tc2_shape(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
+                      const CUtensorMap &zl, const Params &p, int grid, cudaStream_t st) {
+  if constexpr (!Geometry2<NZ, KA>::fits) {
+    return false;
+  } else {
+    constexpr uint32_t smem = Geometry2<NZ, KA>::smem;
+    cudaFuncSetAttribute(krows_tc2_kernel<FAM, NZ, KA>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    krows_tc2_kernel<FAM, NZ, KA><<<grid, kThreads, smem, st>>>(a, c, zh, zl, p);
+    return true;
+  }
+}
+
+template <int FAM>
+bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
+                       const CUtensorMap &zl, const Params &p, int nz, int ka, int grid,
+                       cudaStream_t st) {
+#define SAP_TC2_KA(NZV)                                                             \
+  return ka == 32 ? launch_tc2_shape<FAM, NZV, 32>(a, c, zh, zl, p, grid, st)      \
+                  : launch_tc2_shape<FAM, NZV, 64>(a, c, zh, zl, p, grid, st);
+  switch (nz) {
+    case 32: SAP_TC2_KA(32)
+    case 64: SAP_TC2_KA(64)
+    case 96: SAP_TC2_KA(96)
+    case 128: SAP_TC2_KA(128)
+    default: return false;
+  }
+#undef SAP_TC2_KA
+}
+
+inline bool tc2_fits(int nz, int ka) {
+  if (nz % 32 || nz < 32 || nz > 128 || (ka != 32 && ka != 64)) return false;
+  const uint32_t stage = (NT / 2) * ka * 4 + 2 * 2 * (nz / 2) * 128;
+  const uint32_t fixed = 1024 + 2 * BM * ka * 4 + 512;
+  return (kSmemCap - fixed) / stage >= 3;
+}
+
+}  // namespace tck2
+}  // namespace sap

@@ -160,7 +160,7 @@ class TcPoints:
 
     def gather_rows(self, idx_dev, out=None):
         b = idx_dev.numel()
-        bpad = (b + 127) // 128 * 128
+        bpad = (b + 255) // 256 * 256  # whole 256-row tiles of the CTA-pair kernel
         if out is None:
             out = torch.empty((bpad, self.ka), dtype=torch.float32, device=self.device)
         nat.call("sap_tc_gather_rows", nat.ptr(self.RA), self.ka, nat.ptr(idx_dev), b, bpad,
@@ -173,7 +173,7 @@ class ZOperand:
 
     def __init__(self, m, n, device):
         self.m, self.n = m, n
-        self.nz = (m + 15) // 16 * 16
+        self.nz = (m + 31) // 32 * 32  # the CTA-pair MMA needs N % 32 == 0
         if self.nz > 128:
             raise ContractError("tensor-core path supports at most 128 right-hand sides")
         self.ldz = max(8, (n + 7) // 8 * 8)

@@ -71,7 +71,7 @@ class _Slot:
         self.graph = None  # CUDA graph of the batched power iteration (full batches)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
-        bpad = (b + 127) // 128 * 128
+        bpad = (b + 255) // 256 * 256
         self.RAg = torch.empty((L, bpad, ka), dtype=f32, device=dev) if ka else None
         pin = torch.cuda.is_available()
         self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
