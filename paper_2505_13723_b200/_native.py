@@ -16,7 +16,9 @@ import torch
 
 from .errors import ContractError, NumericalError, WorkerError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsapgp_b200.so")
+# SAP_LIB_PATH selects an alternative build of the same library (kernel tuning sweeps)
+LIB_PATH = os.environ.get("SAP_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libsapgp_b200.so")
 
 SAP_OK, SAP_ERR_CONTRACT, SAP_ERR_NUMERICAL, SAP_ERR_DEVICE = 0, 1, 2, 3
 FAMILY_CODES = {"rbf": 0, "matern32": 1, "matern52": 2}

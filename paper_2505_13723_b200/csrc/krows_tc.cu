@@ -51,8 +51,16 @@ __device__ __forceinline__ float tf32_round(float x) {
   return __uint_as_float(r);
 }
 
+// augmented feature columns a family needs (RBF carries the exp2 offset)
+inline int tc_features(int d, int family) { return 3 * d + 4 + (family == SAP_RBF ? 1 : 0); }
+
+// Row form [zh, zh, zl, nh, nl, 1, 1] and column form [-2zh, -2zl, -2zh, 1, 1,
+// nh, nl] give S = |z_i|^2 + |z_j|^2 - 2 z_i.z_j from a 3-term tf32 split. For
+// RBF (rbf=1) the column form is negated and one more pair (1, 14) is
+// appended, so the tensor core delivers S = 14 - s and the epilogue is a bare
+// exp2 (P = 2^14 k).
 __global__ void build_aug_kernel(const double *X, int64_t n, int d, const double *inv_ls,
-                                 double cfam, int ka, float *RA, float *CA) {
+                                 double cfam, int ka, int rbf, float *RA, float *CA) {
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const double sc = sqrt(cfam);
@@ -65,14 +73,21 @@ __global__ void build_aug_kernel(const double *X, int64_t n, int d, const double
     const float zh = tf32_trunc(float(z));
     const float zl = tf32_round(float(z - double(zh)));
     if (ra) { ra[k] = zh; ra[d + k] = zh; ra[2 * d + k] = zl; }
-    if (ca) { ca[k] = -2.0f * zh; ca[d + k] = -2.0f * zl; ca[2 * d + k] = -2.0f * zh; }
+    const float cs = rbf ? 2.0f : -2.0f;
+    if (ca) { ca[k] = cs * zh; ca[d + k] = cs * zl; ca[2 * d + k] = cs * zh; }
   }
   const float nh = tf32_trunc(float(nrm));
   const float nl = tf32_round(float(nrm - double(nh)));
   const int o = 3 * d;
   if (ra) { ra[o] = nh; ra[o + 1] = nl; ra[o + 2] = 1.0f; ra[o + 3] = 1.0f; }
-  if (ca) { ca[o] = 1.0f; ca[o + 1] = 1.0f; ca[o + 2] = nh; ca[o + 3] = nl; }
-  for (int k = o + 4; k < ka; ++k) {
+  const float sg = rbf ? -1.0f : 1.0f;
+  if (ca) { ca[o] = sg; ca[o + 1] = sg; ca[o + 2] = sg * nh; ca[o + 3] = sg * nl; }
+  const int used = rbf ? o + 5 : o + 4;
+  if (rbf) {
+    if (ra) ra[o + 4] = 1.0f;
+    if (ca) ca[o + 4] = tck::kPExp;
+  }
+  for (int k = used; k < ka; ++k) {
     if (ra) ra[k] = 0.0f;
     if (ca) ca[k] = 0.0f;
   }
@@ -197,13 +212,13 @@ extern "C" {
 
 int sap_tc_points(const double *X, int64_t n, int d, const double *inv_ls, int family, int ka,
                   float *RA, float *CA, void *stream) {
-  if (n < 0 || d < 1 || (ka != 32 && ka != 64) || 3 * d + 4 > ka)
+  if (n < 0 || d < 1 || (ka != 32 && ka != 64) || tc_features(d, family) > ka)
     return fail(SAP_ERR_CONTRACT, "tc_points: d=%d does not fit ka=%d", d, ka);
   const double l2e = 1.4426950408889634;
   double cfam = family == SAP_RBF ? 0.5 * l2e : (family == SAP_MATERN32 ? 3.0 : 5.0) * l2e * l2e;
   if (n == 0) return SAP_OK;
   build_aug_kernel<<<unsigned((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(X, n, d, inv_ls,
-                                                                               cfam, ka, RA, CA);
+                                                                               cfam, ka, family == SAP_RBF, RA, CA);
   return check_launch("build_aug_kernel");
 }
 
@@ -240,9 +255,10 @@ int sap_colabsmax(const float *A, int64_t lda, int64_t n, int m, float *out, voi
 }
 
 int sap_tc_supported(int d, int m) {
-  const int ka = 3 * d + 4 <= 32 ? 32 : 64;
+  const int f = tc_features(d, SAP_RBF);  // the widest family
+  const int ka = f <= 32 ? 32 : 64;
   const int nz = (m + 15) / 16 * 16;
-  return (3 * d + 4 <= 64 && tc_fits(nz, ka)) ? 1 : 0;
+  return (f <= 64 && tc_fits(nz, ka)) ? 1 : 0;
 }
 
 // splits for the CTA-pair kernel: whole waves of 74 pairs over 256-row tiles
@@ -300,7 +316,8 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
     p.debug = dbg ? atoi(dbg) : 0;
   }
   static unsigned long long *prof_buf = nullptr;
-  if (p.debug == 9) {
+  const char *prof_env = getenv("SAP_TC_PROF");
+  if (p.debug == 9 || (prof_env && atoi(prof_env))) {
     if (!prof_buf) cudaMalloc(&prof_buf, 148 * 16 * sizeof(unsigned long long));
     cudaMemsetAsync(prof_buf, 0, 148 * 16 * sizeof(unsigned long long), (cudaStream_t)stream);
     p.prof = prof_buf;

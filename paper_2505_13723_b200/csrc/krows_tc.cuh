@@ -50,6 +50,38 @@ constexpr int kThreads = 384;     // 4 control warps + 2 epilogue warpgroups
 constexpr int kSeg = 16;          // tiles per TMEM accumulator segment
 constexpr float kPScale = 16384.0f;  // 2^14: keeps P's fp16 split out of subnormals
 constexpr float kLn2 = 0.69314718055994531f;
+constexpr float kPExp = 14.0f;         // log2 kPScale, folded into GEMM1 for RBF
+
+// 2^x on the FMA pipe (MUFU is the epilogue's binding unit at 16 lanes/clk/SM
+// against 128 for FFMA): round-to-nearest split x = j + f, f in [-1/2, 1/2],
+// degree-5 fit of 2^f (max rel. error 2.4e-7 in fp32 Horner, the same as
+// ex2.approx), exponent added as an integer. x is floored at -125 so j stays
+// a normal exponent; 2^-125 is far below P's fp16 resolution.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = __fadd_rn(x, 12582912.0f);            // 1.5 * 2^23: j in the low bits
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  float p = fmaf(f, 0.0013276224490255117f, 0.00967553909868002f);
+  p = fmaf(p, f, 0.05550714209675789f);
+  p = fmaf(p, f, 0.24022120237350464f);
+  p = fmaf(p, f, 0.6931469440460205f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
+}
+
+// which of the 32 entries of a TMEM chunk take the polynomial exp2 (measured
+// sweep, config 3: RBF 1/8 of the entries -2%; Matern none -- the epilogue is
+// issue/latency-bound there, not MUFU-bound)
+#ifndef SAP_POLY_RBF_MASK
+#define SAP_POLY_RBF_MASK 0x80808080u
+#endif
+#ifndef SAP_POLY_MAT_MASK
+#define SAP_POLY_MAT_MASK 0x0u
+#endif
+template <int FAM>
+__host__ __device__ constexpr bool poly_entry(int e) {
+  return (((FAM == SAP_RBF ? SAP_POLY_RBF_MASK : SAP_POLY_MAT_MASK) >> e) & 1u) != 0;
+}
 constexpr uint32_t kSmemCap = 227 * 1024;
 
 struct Params {
@@ -86,17 +118,20 @@ __device__ __forceinline__ void split_range(int64_t tiles, int splits, int s, in
   t1 = t0 + q + (s < r ? 1 : 0);
 }
 
-template <int FAM>
+// P = 2^14 k from the GEMM1 output S: for RBF S = 14 - s already (the offset
+// and sign ride in the augmented features, build_aug_kernel); a tiny positive
+// excess from rounding near s = 0 is harmless. Matern: S = s.
+template <int FAM, bool POLY = false>
 __device__ __forceinline__ float pvalue(float s) {
   if constexpr (FAM == SAP_RBF) {
-    return ex2_approx(14.0f - fmaxf(s, 0.0f));
+    return POLY ? ex2_poly(s) : ex2_approx(s);
   } else {
     // the 2^14 scale rides on the polynomial, so ex2 takes -t directly;
     // t = s * rsqrt(s) (MUFU.RSQ, faster than MUFU.SQRT here) with s floored at
     // 1e-30, which also clamps negative rounding, so s <= 0 gives t ~ 0
     s = fmaxf(s, 1e-30f);
     const float t = s * rsqrt_approx(s);
-    const float e = ex2_approx(-t);
+    const float e = POLY ? ex2_poly(-t) : ex2_approx(-t);
     if constexpr (FAM == SAP_MATERN32) {
       return fmaf(t, kPScale * kLn2, kPScale) * e;
     } else {
@@ -105,10 +140,27 @@ __device__ __forceinline__ float pvalue(float s) {
   }
 }
 
+#ifndef SAP_SPLIT_TRUNC
+#define SAP_SPLIT_TRUNC 1
+#endif
+// fp16 hi/lo split of two P values. Truncating the fp32 mantissa to fp16's 11
+// significant bits (LOP3, full-rate ALU) gives a hi that converts exactly and
+// a lo = p - hi that is exact in fp32 before its own rounding, so P_hi + P_lo
+// carries ~2^-23 relative error -- the same as a round-to-nearest hi, without
+// the half-rate f16->f32 back-conversion. (Values under fp16's normal range,
+// P < 2^-14 = 2^-28 of the largest kernel value, lose the exactness; their
+// absolute error is negligible.)
 __device__ __forceinline__ void split2(float p0, float p1, uint32_t &hi, uint32_t &lo) {
+#if SAP_SPLIT_TRUNC
+  const float h0 = __uint_as_float(__float_as_uint(p0) & 0xFFFFE000u);
+  const float h1 = __uint_as_float(__float_as_uint(p1) & 0xFFFFE000u);
+  const __half2 h = __floats2half2_rn(h0, h1);
+  const __half2 l = __floats2half2_rn(__fsub_rn(p0, h0), __fsub_rn(p1, h1));
+#else
   const __half2 h = __floats2half2_rn(p0, p1);
   const float2 hf = __half22float2(h);
   const __half2 l = __floats2half2_rn(p0 - hf.x, p1 - hf.y);
+#endif
   hi = *reinterpret_cast<const uint32_t *>(&h);
   lo = *reinterpret_cast<const uint32_t *>(&l);
 }
@@ -408,9 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2)
-            split2(pvalue<FAM>(__uint_as_float(v[e])), pvalue<FAM>(__uint_as_float(v[e + 1])),
-                   hi[e / 2], lo[e / 2]);
+          for (int e = 0; e < 32; e += 2) {
+            const float x0 = __uint_as_float(v[e]), x1 = __uint_as_float(v[e + 1]);
+            split2(poly_entry<FAM>(e) ? pvalue<FAM, true>(x0) : pvalue<FAM>(x0),
+                   poly_entry<FAM>(e + 1) ? pvalue<FAM, true>(x1) : pvalue<FAM>(x1), hi[e / 2],
+                   lo[e / 2]);
+          }
         }
         tc::st16(taddr, hi);
         tc::st16(taddr + 16, lo);

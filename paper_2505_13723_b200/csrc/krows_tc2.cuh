@@ -26,15 +26,26 @@ using tck::BM;
 using tck::kPScale;
 using tck::kSmemCap;
 using tck::Params;
+using tck::poly_entry;
 using tck::pvalue;
 using tck::split2;
 using tck::split_range;
 using tck::kDescBase;
 
 constexpr int NT = 128;     // points per column tile (64 staged per CTA)
-constexpr int NB = 2;       // S/P tiles in flight in TMEM
-constexpr int kSeg = 8;     // tiles per TMEM accumulator segment
-constexpr int kThreads = 384;
+constexpr int NB = 3;       // S/P tiles in flight in TMEM (columns 0..383)
+constexpr int kSeg = 16;    // tiles per TMEM accumulator segment (2048 points)
+constexpr uint32_t kGCol = NB * NT;  // the (single) accumulator, nz columns
+constexpr int kEpiGroups = 4;                       // epilogue warpgroups
+constexpr int kThreads = 128 * (1 + kEpiGroups);    // + the control warpgroup
+// setmaxnreg split of the registers the launch holds (640 threads x 96): the
+// increases can only draw what the control warpgroup's decrease released,
+// otherwise setmaxnreg.inc spins forever
+constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;
+constexpr int kCtlRegs = 40;
+constexpr int kEpiRegs = 104;
+static_assert(128 * kCtlRegs + 128 * kEpiGroups * kEpiRegs <= kThreads * kLaunchRegs,
+              "setmaxnreg budget exceeds the launch allocation");
 
 template <int NZ, int KA>
 struct Geometry2 {
@@ -47,7 +58,7 @@ struct Geometry2 {
   static constexpr uint32_t stages_raw = (kSmemCap - fixed) / stage_bytes;
   static constexpr uint32_t STAGES = stages_raw > 8 ? 8 : stages_raw;
   static constexpr uint32_t smem = fixed + STAGES * stage_bytes;
-  static constexpr bool fits = STAGES >= 3 && NZ % 32 == 0 && NZ >= 32 && NZ <= 128;
+  static constexpr bool fits = STAGES >= 3 && NZ % 16 == 0 && NZ >= 16 && kGCol + NZ <= 512;
 };
 
 template <int FAM, int NZ, int KA>
@@ -77,9 +88,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t *a_empty = a_full + 2;         // [2]       both
   uint64_t *s_full = a_empty + 2;         // [NB]      both
   uint64_t *p_full = s_full + NB;         // [NB]      leader: 16 warp arrivals
-  uint64_t *g_full = p_full + NB;         // [2]       both
-  uint64_t *g_empty = g_full + 2;         // [2]       leader: 16 warp arrivals
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(g_empty + 2);
+  uint64_t *g_full = p_full + NB;         // [1]       both
+  uint64_t *g_empty = g_full + 1;         // [1]       leader: 16 warp arrivals
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(g_empty + 1);
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < STAGES; ++s) {
@@ -88,14 +99,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int k = 0; k < NB; ++k) {
       tc::mbar_init(tc::smem_u32(&s_full[k]), 1);
-      tc::mbar_init(tc::smem_u32(&p_full[k]), 16);
+      tc::mbar_init(tc::smem_u32(&p_full[k]), 8 * kEpiGroups);
     }
     for (int k = 0; k < 2; ++k) {
       tc::mbar_init(tc::smem_u32(&a_full[k]), 1);
       tc::mbar_init(tc::smem_u32(&a_empty[k]), 1);
-      tc::mbar_init(tc::smem_u32(&g_full[k]), 1);
-      tc::mbar_init(tc::smem_u32(&g_empty[k]), 16);
     }
+    tc::mbar_init(tc::smem_u32(g_full), 1);
+    tc::mbar_init(tc::smem_u32(g_empty), 8 * kEpiGroups);
     tc::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -115,6 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const int units = p.row_tiles * p.splits;  // row_tiles counts 256-row pair tiles here
 
+  if (warp < 4) tc::setmaxnreg_dec<kCtlRegs>();
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (tc::elect_one()) {
@@ -187,6 +199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::mbar_wait(tc::smem_u32(&a_full[ab]), (uc >> 1) & 1);
         tc::fence_after();
         const uint64_t a_desc = a_desc0 + ((ab * Geo::a_bytes) >> 4);
+        int g1 = 0;  // GEMM1s issued in this unit
         auto gemm1 = [&]() {
           cc = clock64();
           tc::mbar_wait(full0 + 8 * s1, ph1);
@@ -204,28 +217,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc::commit_pair(sfull0 + 8 * r1);
           i1 += clock64() - cw;
           if (++s1 == STAGES) { s1 = 0; ph1 ^= 1; }
-          r1 = (r1 + 1) & (NB - 1);
+          if (++r1 == NB) r1 = 0;
+          if (++g1 == nt) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
         };
-        if (nt > 0) gemm1();
-        if (nt == 1) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
-        uint32_t g_tmem = 0;
+        const uint32_t g_tmem = tmem + kGCol;
         int seg_j = 0;
         for (int j = 0; j < nt; ++j) {
-          // GEMM1 of the next tile goes first: it overwrites the S/P buffer of
-          // tile j-1, whose GEMM2 was issued earlier (in-order tensor pipe), and
-          // runs while the epilogue converts tile j
-          if (j + 1 < nt) {
-            gemm1();
-            if (j + 2 == nt) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
-          }
+          // GEMM1 runs up to NB-1 tiles ahead: GEMM1(j+NB-1) overwrites the
+          // S/P slot of tile j-1, whose GEMM2 was issued earlier (in-order
+          // tensor pipe), so the epilogue converts while GEMM2 streams
+          while (g1 < nt && g1 <= j + NB - 1) gemm1();
           const bool seg_first = seg_j == 0;
           const bool seg_last = seg_j == kSeg - 1 || j + 1 == nt;
           cc = clock64();
-          if (seg_first) {
-            const int gb = sc & 1;
-            tc::mbar_wait_cluster(tc::smem_u32(&g_empty[gb]), ((sc >> 1) & 1) ^ 1);
-            g_tmem = tmem + 256 + gb * NZ;
-          }
+          if (seg_first) tc::mbar_wait_cluster(tc::smem_u32(g_empty), (sc & 1) ^ 1);
           const unsigned long long cg = clock64();
           wg += cg - cc;
           tc::mbar_wait_cluster(pfull0 + 8 * r2, ph2);
@@ -248,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           tc::commit_pair(empty0 + 8 * s2);
           if (seg_last) {
-            tc::commit_pair(tc::smem_u32(&g_full[sc & 1]));
+            tc::commit_pair(tc::smem_u32(g_full));
             ++sc;
             seg_j = 0;
           } else {
@@ -256,8 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           i2 += clock64() - cp;
           if (++s2 == STAGES) s2 = 0;
-          r2 = (r2 + 1) & (NB - 1);
-          if (r2 == 0) ph2 ^= 1;
+          if (++r2 == NB) { r2 = 0; ph2 ^= 1; }
         }
       }
       if (p.prof) {
@@ -270,52 +274,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs) =====================
-    // Both warpgroups work on every tile: warpgroup h converts S columns
-    // [64h, 64h+64) and drains accumulator columns [h*nz/2, (h+1)*nz/2).
-    // (A ping-pong split -- each warpgroup owning alternate tiles -- measured
-    // 15% slower: with a 2-deep S ring it loses GEMM1's one-tile lookahead.)
+    // Four warpgroups, i.e. four warps per SM sub-partition, so TMEM load/store
+    // and dependency latencies hide behind the other warps' MUFU/FMA work:
+    // warpgroup w converts S columns [32w, 32w+32) of every tile and drains the
+    // accumulator's 8-column granules w, w+4, w+8, ... at every segment end.
+    tc::setmaxnreg_inc<kEpiRegs>();
     const int q = warp & 3;
-    const int h = (warp - 4) >> 2;
+    const int w = (warp - 4) >> 2;
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_off = uint32_t(q * 32) << 16;
-    constexpr int NACC = NZ / 2;            // accumulator columns per warpgroup
-    const int g0 = h * NACC;
+    constexpr int NGRAN = NZ / 8;                           // 8-column accumulator granules
+    constexpr int NMINE = (NGRAN + kEpiGroups - 1) / kEpiGroups;
+    const int ngran = (NGRAN - w + kEpiGroups - 1) / kEpiGroups;  // granules of this warpgroup
     const uint32_t sfull0 = tc::smem_u32(s_full);
     const uint32_t pfull_leader = tc::mapa(tc::smem_u32(p_full), 0);
     const uint32_t gempty_leader = tc::mapa(tc::smem_u32(g_empty), 0);
     uint32_t r = 0, ph = 0, sc = 0;
-    float acc[NACC];
+    float acc[NMINE * 8];
 #pragma unroll
-    for (int c = 0; c < NACC; ++c) acc[c] = 0.0f;
+    for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
     bool pend = false, pend_last = false, pend_live = false;
     float *pend_dst = nullptr;
     unsigned long long es = 0, ec = 0, ed = 0, ea = 0, ce;
     auto drain = [&]() {  // add a finished TMEM segment, one tile late
-      const int gb = sc & 1;
-      tc::mbar_wait(tc::smem_u32(&g_full[gb]), (sc >> 1) & 1);
+      tc::mbar_wait(tc::smem_u32(g_full), sc & 1);
       tc::fence_after();
-      const uint32_t gbase = tmem + lane_off + 256 + gb * NZ + g0;
+      const uint32_t gbase = tmem + lane_off + kGCol;
 #pragma unroll
-      for (int c0 = 0; c0 < NACC; c0 += 16) {
-        uint32_t v[16];
-        tc::ld16(gbase + c0, v);
-        tc::wait_ld();
+      for (int k = 0; k < NMINE; ++k) {
+        if (k < ngran) {
+          uint32_t v[8];
+          tc::ld8(gbase + (w + k * kEpiGroups) * 8, v);
+          tc::wait_ld();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) acc[c0 + e] += __uint_as_float(v[e]);
+          for (int e = 0; e < 8; ++e) acc[k * 8 + e] += __uint_as_float(v[e]);
+        }
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(gempty_leader + 8 * gb);
+      if (lane == 0) tc::mbar_arrive_cluster(gempty_leader);
       ++sc;
       pend = false;
       if (pend_last) {
         if (pend_live) {
 #pragma unroll
-          for (int c = 0; c < NACC; ++c)
-            if (g0 + c < p.m) pend_dst[g0 + c] = acc[c];
+          for (int k = 0; k < NMINE; ++k)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int c = (w + k * kEpiGroups) * 8 + e;
+              if (k < ngran && c < p.m) pend_dst[c] = acc[k * 8 + e];
+            }
         }
 #pragma unroll
-        for (int c = 0; c < NACC; ++c) acc[c] = 0.0f;
+        for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
       }
     };
     for (int u = pair; u < units; u += npairs) {
@@ -326,8 +337,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool live = grow < p.b;
       float *dst = p.part + (int64_t(split) * p.b + (live ? grow : 0)) * p.m;
       const int64_t rid = (p.row_ids && live) ? p.row_ids[grow] : INT64_MIN;
-      if (t1 == t0 && live)
-        for (int c = g0; c < g0 + NACC && c < p.m; ++c) dst[c] = 0.0f;
+      if (t1 == t0 && live) {
+        for (int k = 0; k < ngran; ++k)
+          for (int e = 0; e < 8; ++e) {
+            const int c = (w + k * kEpiGroups) * 8 + e;
+            if (c < p.m) dst[c] = 0.0f;
+          }
+      }
       int seg_j = 0;
       for (int64_t t = t0; t < t1; ++t) {
         ce = clock64();
@@ -335,48 +351,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::fence_after();
         const unsigned long long cs = clock64();
         es += cs - ce;
-        // both 32-column chunks of this warpgroup are loaded before any math, so
-        // the second load's latency hides under the first chunk's MUFU work
-        const uint32_t tbase = tmem + lane_off + r * NT + h * 64;
-        uint32_t va[32], vb[32];
-        tc::ld32(tbase, va);
-        tc::ld32(tbase + 32, vb);
-        tc::wait_ld();
-        const int64_t dc64 = rid - (p.col_base + t * NT) - h * 64;
-        const bool diag = dc64 >= 0 && dc64 < 64;
+        const uint32_t taddr = tmem + lane_off + r * NT + w * 32;
+        uint32_t v[32];
+        tc::ld32(taddr, v);
+        const int64_t dc64 = rid - (p.col_base + t * NT) - w * 32;
+        const bool diag = dc64 >= 0 && dc64 < 32;
         const int dc = int(dc64);
-        auto convert = [&](const uint32_t (&v)[32], int off, uint32_t taddr) {
-          uint32_t o[32];  // P_hi (16 packed words) then P_lo over the 32 columns
-          if (p.debug == 1 || p.debug == 4) {
+        tc::wait_ld();
+        uint32_t o[32];  // P_hi (16 packed words) then P_lo over the 32 columns
+        if (p.debug == 1 || p.debug == 3 || p.debug == 4) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = v[e];
-          } else if (__any_sync(0xffffffffu, diag)) {
+          for (int e = 0; e < 32; ++e) o[e] = v[e];
+        } else if (__any_sync(0xffffffffu, diag)) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              float p0 = pvalue<FAM>(__uint_as_float(v[e]));
-              float p1 = pvalue<FAM>(__uint_as_float(v[e + 1]));
-              if (diag && dc == off + e) p0 = kPScale;
-              if (diag && dc == off + e + 1) p1 = kPScale;
-              split2(p0, p1, o[e / 2], o[16 + e / 2]);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; e += 2)
-              split2(pvalue<FAM>(__uint_as_float(v[e])), pvalue<FAM>(__uint_as_float(v[e + 1])),
-                     o[e / 2], o[16 + e / 2]);
+          for (int e = 0; e < 32; e += 2) {
+            float p0 = pvalue<FAM>(__uint_as_float(v[e]));
+            float p1 = pvalue<FAM>(__uint_as_float(v[e + 1]));
+            if (diag && dc == e) p0 = kPScale;
+            if (diag && dc == e + 1) p1 = kPScale;
+            split2(p0, p1, o[e / 2], o[16 + e / 2]);
           }
-          tc::st32(taddr, o);
-        };
-        convert(va, 0, tbase);
-        convert(vb, 32, tbase + 32);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float x0 = __uint_as_float(v[e]), x1 = __uint_as_float(v[e + 1]);
+            split2(poly_entry<FAM>(e) ? pvalue<FAM, true>(x0) : pvalue<FAM>(x0),
+                   poly_entry<FAM>(e + 1) ? pvalue<FAM, true>(x1) : pvalue<FAM>(x1),
+                   o[e / 2], o[16 + e / 2]);
+          }
+        }
+        tc::st32(taddr, o);
         tc::wait_st();
         tc::fence_before();
         __syncwarp();
         const unsigned long long cw2 = clock64();
         ec += cw2 - cs;
         if (lane == 0) tc::mbar_arrive_cluster(pfull_leader + 8 * r);
-        r = (r + 1) & (NB - 1);
-        if (r == 0) ph ^= 1;
+        if (++r == NB) { r = 0; ph ^= 1; }
         const unsigned long long ca = clock64();
         ea += ca - cw2;
         if (pend) drain();
@@ -430,9 +441,13 @@ bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtenso
   return ka == 32 ? launch_tc2_shape<FAM, NZV, 32>(a, c, zh, zl, p, grid, st)      \
                   : launch_tc2_shape<FAM, NZV, 64>(a, c, zh, zl, p, grid, st);
   switch (nz) {
+    case 16: SAP_TC2_KA(16)
     case 32: SAP_TC2_KA(32)
+    case 48: SAP_TC2_KA(48)
     case 64: SAP_TC2_KA(64)
+    case 80: SAP_TC2_KA(80)
     case 96: SAP_TC2_KA(96)
+    case 112: SAP_TC2_KA(112)
     case 128: SAP_TC2_KA(128)
     default: return false;
   }
@@ -440,7 +455,7 @@ bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtenso
 }
 
 inline bool tc2_fits(int nz, int ka) {
-  if (nz % 32 || nz < 32 || nz > 128 || (ka != 32 && ka != 64)) return false;
+  if (nz % 16 || nz < 16 || kGCol + nz > 512 || (ka != 32 && ka != 64)) return false;
   const uint32_t stage = (NT / 2) * ka * 4 + 2 * 2 * (nz / 2) * 128;
   const uint32_t fixed = 1024 + 2 * BM * ka * 4 + 512;
   return (kSmemCap - fixed) / stage >= 3;

@@ -144,9 +144,10 @@ class TcPoints:
                              dtype=torch.float64).to(device).contiguous()
         n, d = Xd.shape
         hi = n if hi is None else hi
-        self.ka = 32 if 3 * d + 4 <= 32 else 64
-        if 3 * d + 4 > 64:
-            raise ContractError(f"tensor-core path supports d <= 20 (got d={d})")
+        feats = 3 * d + 4 + (1 if spec.family == "rbf" else 0)  # krows_tc.cu tc_features
+        self.ka = 32 if feats <= 32 else 64
+        if feats > 64:
+            raise ContractError(f"tensor-core path supports d <= 19 (got d={d})")
         inv = torch.as_tensor(np.broadcast_to(1.0 / spec.lengthscales, (d,)).copy(), device=device)
         self.RA = torch.empty((max(n, 1), self.ka), dtype=torch.float32, device=device)
         self.CA = torch.empty((max(hi - lo, 1), self.ka), dtype=torch.float32, device=device)
@@ -173,7 +174,7 @@ class ZOperand:
 
     def __init__(self, m, n, device):
         self.m, self.n = m, n
-        self.nz = (m + 31) // 32 * 32  # the CTA-pair MMA needs N % 32 == 0
+        self.nz = (m + 15) // 16 * 16  # MMA N granularity of the CTA pair
         if self.nz > 128:
             raise ContractError("tensor-core path supports at most 128 right-hand sides")
         self.ldz = max(8, (n + 7) // 8 * 8)
