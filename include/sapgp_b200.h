@@ -24,7 +24,7 @@
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
- *   sap_krows_tc (+ sap_tc_points, sap_tc_gather_rows, sap_z_operand)
+ *   sap_krows_tc (+ sap_tc_points, sap_tc_gather_rows, sap_tc_gather_cols, sap_z_operand)
  *                       <- the same col_dist_matmul product on the 5th-gen
  *                          tensor cores (the solver's Phase I, solvers.py:377)
  *
@@ -137,10 +137,16 @@ int sap_tc_points(const double *X, int64_t n, int d, const double *inv_ls, int f
 int sap_tc_gather_rows(const float *RA, int ka, const int64_t *idx, int64_t b, int64_t bpad,
                        float *out, void *stream);
 
+/* Column-form features (CA layout) of the points idx[0..b), rebuilt exactly
+ * from their row form RA; rows b..bpad-1 are zero. */
+int sap_tc_gather_cols(const float *RA, int ka, int d, int family, const int64_t *idx, int64_t b,
+                       int64_t bpad, float *out, void *stream);
+
 /*
  * Z operand of the tensor-core product: Zhi/Zlo (fp16, [nz][ldz]) = split of
  * scale_c * (zp*P + zq*Q) with scale_c a power of two from the bounds Pb/Qb
- * (zscale[c] receives it). Q/Qb may be NULL.
+ * (zscale[c] receives it), for rows c < m. Rows m..nz-1 (MMA padding) are
+ * not written: the caller zeroes them once. Q/Qb may be NULL.
  */
 int sap_z_operand(const float *P, const float *Q, int64_t ldp, int64_t n, int m, double zp,
                   double zq, const float *Pb, const float *Qb, int nz, int64_t ldz, void *Zhi,

@@ -48,6 +48,7 @@ SIGNATURES = {
     "sap_combine": (_I, [_P, _I64, _P, _P, _I64, _I64, _I, _D, _D, _P]),
     "sap_tc_points": (_I, [_P, _I64, _I, _P, _I, _I, _P, _P, _P]),
     "sap_tc_gather_rows": (_I, [_P, _I, _P, _I64, _I64, _P, _P]),
+    "sap_tc_gather_cols": (_I, [_P, _I, _I, _I, _P, _I64, _I64, _P, _P]),
     "sap_z_operand": (_I, [_P, _P, _I64, _I64, _I, _D, _D, _P, _P, _I, _I64, _P, _P, _P, _P]),
     "sap_colabsmax": (_I, [_P, _I64, _I64, _I, _P, _P]),
     "sap_krows_tc_workspace": (_SZ, [_I64, _I, _I64]),

@@ -101,28 +101,105 @@ __global__ void gather_rows_kernel(const float *RA, int ka, const int64_t *idx, 
   out[e] = i < b ? RA[idx[i] * ka + (e % ka)] : 0.0f;
 }
 
+// column form of gathered points rebuilt from their row form (build_aug_kernel
+// layouts; every step is a sign flip or a factor of 2, so it is exact): lets a
+// block of points serve as the column set of a product (the Nystrom sketch
+// K[B,B] Omega) without a column-form copy of every point
+__global__ void gather_cols_kernel(const float *RA, int ka, int d, int rbf, const int64_t *idx,
+                                   int64_t b, int64_t bpad, float *out) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= bpad * ka) return;
+  const int64_t i = e / ka;
+  const int k = int(e % ka);
+  float v = 0.0f;
+  if (i < b) {
+    const float *ra = RA + idx[i] * ka;
+    const float cs = rbf ? 2.0f : -2.0f, sg = rbf ? -1.0f : 1.0f;
+    const int o = 3 * d;
+    if (k < d) v = cs * ra[k];                      // -2 zh   (x row zh)
+    else if (k < 2 * d) v = cs * ra[d + k];         // -2 zl   (x row zh): ra[2d + (k-d)]
+    else if (k < o) v = cs * ra[k - d];             // -2 zh   (x row zl): ra[d + (k-2d)]
+    else if (k == o || k == o + 1) v = sg;          // 1       (x row nh, nl)
+    else if (k == o + 2) v = sg * ra[o];            // nh      (x row 1)
+    else if (k == o + 3) v = sg * ra[o + 1];        // nl      (x row 1)
+    else if (k == o + 4 && rbf) v = tck::kPExp;     // 14      (x row 1)
+  }
+  out[e] = v;
+}
+
 // Z operand: ZT_hi/ZT_lo[c][j] = fp16 split of scale_c * (zp P[c][j] + zq Q[c][j]),
 // scale_c = 2^floor(log2(16384 / bound_c)) from per-column magnitude bounds.
-__global__ void z_operand_kernel(const float *P, const float *Q, int64_t ldp, int64_t n, int m,
-                                 float zp, float zq, const float *Pb, const float *Qb, int nz,
+// Rows c >= m (MMA padding) are not touched: the caller zeroes them once.
+__device__ __forceinline__ float z_scale(float zp, float zq, const float *Pb, const float *Qb,
+                                         bool hasq, int c) {
+  const float bound = fabsf(zp) * Pb[c] + (hasq ? fabsf(zq) * Qb[c] : 0.0f);
+  float sc = 1.0f;
+  if (bound > 0.0f && isfinite(bound)) sc = exp2f(floorf(log2f(16384.0f / bound)));
+  return fminf(fmaxf(sc, 0x1p-100f), 0x1p100f);
+}
+
+__device__ __forceinline__ void z_split(float z, __half &h, __half &l) {
+  h = __float2half_rn(z);
+  l = __float2half_rn(z - __half2float(h));
+}
+
+// vectorised form: 8 consecutive points per thread (2 x float4 from P and Q,
+// one 16-byte store each to Zhi and Zlo); needs 16-byte aligned rows
+__global__ void z_operand_vec_kernel(const float *P, const float *Q, int64_t ldp, int64_t n,
+                                     float zp, float zq, const float *Pb, const float *Qb,
+                                     int64_t ldz, __half *Zhi, __half *Zlo, float *zscale) {
+  const int c = blockIdx.y;
+  const float sc = z_scale(zp, zq, Pb, Qb, Q != nullptr, c);
+  if (blockIdx.x == 0 && threadIdx.x == 0) zscale[c] = sc;
+  const float a = zp * sc, bq = zq * sc;
+  const float *pr = P + int64_t(c) * ldp;
+  const float *qr = Q ? Q + int64_t(c) * ldp : nullptr;
+  for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; j < ldz;
+       j += int64_t(gridDim.x) * blockDim.x * 8) {
+    float z[8];
+    if (j + 8 <= n) {
+      const float4 p0 = *reinterpret_cast<const float4 *>(pr + j);
+      const float4 p1 = *reinterpret_cast<const float4 *>(pr + j + 4);
+      z[0] = a * p0.x; z[1] = a * p0.y; z[2] = a * p0.z; z[3] = a * p0.w;
+      z[4] = a * p1.x; z[5] = a * p1.y; z[6] = a * p1.z; z[7] = a * p1.w;
+      if (qr) {
+        const float4 q0 = *reinterpret_cast<const float4 *>(qr + j);
+        const float4 q1 = *reinterpret_cast<const float4 *>(qr + j + 4);
+        z[0] = fmaf(bq, q0.x, z[0]); z[1] = fmaf(bq, q0.y, z[1]);
+        z[2] = fmaf(bq, q0.z, z[2]); z[3] = fmaf(bq, q0.w, z[3]);
+        z[4] = fmaf(bq, q1.x, z[4]); z[5] = fmaf(bq, q1.y, z[5]);
+        z[6] = fmaf(bq, q1.z, z[6]); z[7] = fmaf(bq, q1.w, z[7]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int64_t jj = j + e;
+        z[e] = jj < n ? (qr ? fmaf(bq, qr[jj], a * pr[jj]) : a * pr[jj]) : 0.0f;
+      }
+    }
+    __align__(16) __half h[8], l[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) z_split(z[e], h[e], l[e]);
+    *reinterpret_cast<uint4 *>(Zhi + int64_t(c) * ldz + j) = *reinterpret_cast<const uint4 *>(h);
+    *reinterpret_cast<uint4 *>(Zlo + int64_t(c) * ldz + j) = *reinterpret_cast<const uint4 *>(l);
+  }
+}
+
+__global__ void z_operand_kernel(const float *P, const float *Q, int64_t ldp, int64_t n,
+                                 float zp, float zq, const float *Pb, const float *Qb,
                                  int64_t ldz, __half *Zhi, __half *Zlo, float *zscale) {
   const int c = blockIdx.y;
-  float bound = fabsf(zp) * Pb[c] + (Q ? fabsf(zq) * Qb[c] : 0.0f);
-  float sc = 1.0f;
-  if (c < m && bound > 0.0f && isfinite(bound)) sc = exp2f(floorf(log2f(16384.0f / bound)));
-  sc = fminf(fmaxf(sc, 0x1p-100f), 0x1p100f);
+  const float sc = z_scale(zp, zq, Pb, Qb, Q != nullptr, c);
   if (blockIdx.x == 0 && threadIdx.x == 0) zscale[c] = sc;
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ldz;
        j += int64_t(gridDim.x) * blockDim.x) {
     float z = 0.0f;
-    if (c < m && j < n) {
+    if (j < n) {
       z = zp * P[int64_t(c) * ldp + j];
       if (Q) z = fmaf(zq, Q[int64_t(c) * ldp + j], z);
       z *= sc;
     }
-    const __half h = __float2half_rn(z);
-    Zhi[int64_t(c) * ldz + j] = h;
-    Zlo[int64_t(c) * ldz + j] = __float2half_rn(z - __half2float(h));
+    z_split(z, Zhi[int64_t(c) * ldz + j], Zlo[int64_t(c) * ldz + j]);
   }
 }
 
@@ -231,16 +308,37 @@ int sap_tc_gather_rows(const float *RA, int ka, const int64_t *idx, int64_t b, i
   return check_launch("gather_rows_kernel");
 }
 
+int sap_tc_gather_cols(const float *RA, int ka, int d, int family, const int64_t *idx,
+                       int64_t b, int64_t bpad, float *out, void *stream) {
+  if (b <= 0 || bpad < b || tc_features(d, family) > ka)
+    return fail(SAP_ERR_CONTRACT, "tc_gather_cols: bad shape");
+  const int64_t tot = bpad * ka;
+  gather_cols_kernel<<<unsigned((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      RA, ka, d, family == SAP_RBF, idx, b, bpad, out);
+  return check_launch("gather_cols_kernel");
+}
+
 int sap_z_operand(const float *P, const float *Q, int64_t ldp, int64_t n, int m, double zp,
                   double zq, const float *Pb, const float *Qb, int nz, int64_t ldz, void *Zhi,
                   void *Zlo, float *zscale, void *stream) {
   if (m <= 0 || nz < m || nz % 16 || ldz < n || ldz % 8)
     return fail(SAP_ERR_CONTRACT, "z_operand: bad shape m=%d nz=%d ldz=%lld", m, nz,
                 (long long)ldz);
-  dim3 grid(unsigned(std::min<int64_t>((ldz + 255) / 256, 256)), unsigned(nz));
-  z_operand_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      P, Q, ldp, n, m, float(zp), float(zq), Pb, Qb, nz, ldz, static_cast<__half *>(Zhi),
-      static_cast<__half *>(Zlo), zscale);
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool vec = ldp % 4 == 0 && al16(P) && (!Q || al16(Q)) && al16(Zhi) && al16(Zlo);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (vec) {
+    const int64_t groups = ldz / 8;
+    dim3 grid(unsigned(std::min<int64_t>((groups + 255) / 256, 1024)), unsigned(m));
+    z_operand_vec_kernel<<<grid, 256, 0, st>>>(P, Q, ldp, n, float(zp), float(zq), Pb, Qb, ldz,
+                                               static_cast<__half *>(Zhi),
+                                               static_cast<__half *>(Zlo), zscale);
+    return check_launch("z_operand_vec_kernel");
+  }
+  dim3 grid(unsigned(std::min<int64_t>((ldz + 255) / 256, 256)), unsigned(m));
+  z_operand_kernel<<<grid, 256, 0, st>>>(P, Q, ldp, n, float(zp), float(zq), Pb, Qb, ldz,
+                                         static_cast<__half *>(Zhi), static_cast<__half *>(Zlo),
+                                         zscale);
   return check_launch("z_operand_kernel");
 }
 

@@ -158,6 +158,16 @@ class TcPoints:
                 nat.call("sap_tc_points", nat.ptr(Xd[lo:hi]), hi - lo, d, nat.ptr(inv), spec.code,
                          self.ka, None, nat.ptr(self.CA), nat.stream_handle())
         self.lo, self.hi, self.n, self.d, self.device = lo, hi, n, d, device
+        self.code = spec.code
+
+    def gather_cols(self, idx_dev, out=None):
+        """Column-form features of the points idx (any ids, not only this shard)."""
+        b = idx_dev.numel()
+        if out is None:
+            out = torch.empty((b, self.ka), dtype=torch.float32, device=self.device)
+        nat.call("sap_tc_gather_cols", nat.ptr(self.RA), self.ka, self.d, self.code,
+                 nat.ptr(idx_dev), b, out.shape[0], nat.ptr(out), nat.stream_handle())
+        return out
 
     def gather_rows(self, idx_dev, out=None):
         b = idx_dev.numel()
@@ -178,8 +188,9 @@ class ZOperand:
         if self.nz > 128:
             raise ContractError("tensor-core path supports at most 128 right-hand sides")
         self.ldz = max(8, (n + 7) // 8 * 8)
-        self.hi = torch.empty((self.nz, self.ldz), dtype=torch.float16, device=device)
-        self.lo = torch.empty((self.nz, self.ldz), dtype=torch.float16, device=device)
+        # rows m..nz-1 are MMA padding: zeroed here once, never rewritten
+        self.hi = torch.zeros((self.nz, self.ldz), dtype=torch.float16, device=device)
+        self.lo = torch.zeros((self.nz, self.ldz), dtype=torch.float16, device=device)
         self.scale = torch.ones(self.nz, dtype=torch.float32, device=device)
         self.bound = torch.zeros(self.nz, dtype=torch.float32, device=device)
 
@@ -195,14 +206,17 @@ class ZOperand:
         return self
 
 
-def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False):
-    """out (b x m fp32) = variance * K(rows, shard columns) @ Z on the tensor cores."""
-    ncols = tcp.hi - tcp.lo
+def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False, cols=None):
+    """out (b x m fp32) = variance * K(rows, shard columns) @ Z on the tensor cores.
+    ``cols`` = (CA, col_base) replaces the shard's column features (e.g. a
+    gathered block, with row_ids given as positions in it)."""
+    CA, col_base = (tcp.CA, tcp.lo) if cols is None else cols
+    ncols = (tcp.hi - tcp.lo) if cols is None else CA.shape[0]
     need = nat.load().sap_krows_tc_workspace(b, zop.m, ncols)
     if ws is None or ws.numel() * 4 < need:
         ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=tcp.device)
-    nat.call("sap_krows_tc", nat.ptr(tcp.CA), ncols, tcp.ka, nat.ptr(RAg), RAg.shape[0],
-             nat.ptr(row_ids), b, tcp.lo, nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz,
+    nat.call("sap_krows_tc", nat.ptr(CA), ncols, tcp.ka, nat.ptr(RAg), RAg.shape[0],
+             nat.ptr(row_ids), b, col_base, nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz,
              nat.ptr(zop.scale), zop.m, spec.code, spec.variance, nat.ptr(out), out.stride(0),
              int(accumulate), nat.ptr(ws), ws.numel() * 4, nat.stream_handle())
     return out
@@ -257,7 +271,10 @@ class KernelOracle:
         self.X = Xn
         self.lam = float(lam)
         self.device = _device(device)
-        self.points = DevicePoints(spec, Xn, self.device)
+        # one host->device copy of X (fp64); the FFMA and tensor-core point
+        # formats are both derived from it on the device
+        self._Xd = torch.as_tensor(Xn, dtype=torch.float64).to(self.device).contiguous()
+        self.points = DevicePoints(spec, self._Xd, self.device)
         self._ws = None
         self._tc = None
         self.backend = "auto"  # "tc" (tcgen05), "ffma", or "auto" (tc when the shape fits)
@@ -265,7 +282,7 @@ class KernelOracle:
     def tc_points(self, lo=0, hi=None):
         hi = self.n if hi is None else hi
         if self._tc is None or (self._tc.lo, self._tc.hi) != (lo, hi):
-            self._tc = TcPoints(self.spec, self.X, self.device, lo, hi)
+            self._tc = TcPoints(self.spec, self._Xd, self.device, lo, hi)
         return self._tc
 
     def use_tc(self, m):

@@ -11,13 +11,14 @@ block-row product and the update depends only on (seed, t) and X:
     eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
                                    10, substream(seed, "power", t)) :389-396
 
-so they are produced ``L = config.lookahead`` iterations at a time, on a
-side CUDA stream and a host worker thread, while the main stream runs the
-previous batch's block-row products. Per batch there is one device->host
+so they are produced in batches on a side CUDA stream and a host worker
+thread, up to two batches ahead of the main stream's block-row products.
+Batch sizes ramp 1, 2, 4, ... up to ``L = config.lookahead`` so the first
+iteration waits for one plan only, not for a full batch. Per batch there is one device->host
 round trip (three r x r matrices per iteration) for the host LAPACK part
 (``randnla.factor_core_retry``); everything dimension-b runs on the GPU in
 fp64 (QR of the sketch, U = Qs Ur, the batched power iteration). Buffers
-live in two preallocated slots reused under CUDA events, so nothing is
+live in three preallocated slots reused under CUDA events, so nothing is
 allocated in steady state.
 """
 
@@ -104,8 +105,8 @@ class Lookahead:
                  tcp=None):
         self.o, self.shard, self.seed = oracle, shard, seed
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
-        # two slots of L fp64 b x b blocks: keep them under ~2 GB
-        cap = max(1, int(2e9 // (2 * 8 * b * b)))
+        # three slots of L fp64 b x b blocks: keep them under ~3 GB
+        cap = max(1, int(3e9 // (3 * 8 * b * b)))
         self.total, self.L = total, max(1, min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
@@ -115,7 +116,23 @@ class Lookahead:
         self.side = torch.cuda.Stream(device=dev, priority=-1)
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
-        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(2)]
+        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(3)]
+        # side-stream scratch of the tensor-core sketch (used one plan at a time)
+        # (only for blocks of >= 512 points: below that the 256-row tiles are
+        # mostly padding and the FFMA sketch, ~4x more precise, costs little)
+        self.sk_zop = None
+        if tcp is not None and self.r and b >= 512 and oracle.use_tc(self.r):
+            self.sk_zop = K.ZOperand(self.r, b, dev)
+            self.sk_cols = torch.empty((b, ka), dtype=torch.float32, device=dev)
+            self.sk_pos = torch.arange(b, dtype=torch.int64, device=dev)
+            need = K.nat.load().sap_krows_tc_workspace(b, self.r, b)
+            self.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
+        # batch k covers iterations [bounds[k], bounds[k+1])
+        self.bounds = [0]
+        c = 1
+        while self.bounds[-1] < total:
+            self.bounds.append(min(total, self.bounds[-1] + c))
+            c = min(2 * c, self.L)
         self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sap-lookahead")
         # host workers for the per-iteration numpy RNG and r x r LAPACK work (both
         # release the GIL in their kernels); sized to leave cores for the main thread
@@ -134,7 +151,7 @@ class Lookahead:
         except Exception:  # pragma: no cover - threadpoolctl is optional
             self._blas_limit = None
         self.cur = None
-        self.k = 0
+        self.k = -1  # batch currently consumed
         # capture both slots' power-iteration graphs up front (static buffers; the
         # values are filled per batch), so no capture lands inside a timed solve
         if self.L > 1:
@@ -148,7 +165,13 @@ class Lookahead:
                                           capture_error_mode="thread_local"):
                         self._power(slot, self.L)
                     slot.bad.zero_()
-        self.fut = self.pool.submit(self._produce, self.slots[0], 0, min(self.L, total))
+        self.futs = {}
+        for k in range(min(2, len(self.bounds) - 1)):
+            self._submit(k)
+
+    def _submit(self, k):
+        t0, t1 = self.bounds[k], self.bounds[k + 1]
+        self.futs[k] = self.pool.submit(self._produce, self.slots[k % 3], t0, t1 - t0)
 
     def close(self):
         self.pool.shutdown(wait=True)
@@ -165,15 +188,13 @@ class Lookahead:
             if cur is not None:
                 ev = torch.cuda.Event()
                 ev.record(main)
-                cur.slot.free = ev
-            cur = self.fut.result()
+                cur.slot.free = ev  # batch k+2 refills this slot after it
+            self.k += 1
+            cur = self.futs.pop(self.k).result()
             main.wait_event(cur.ready)
             self.cur = cur
-            self.k += 1
-            nxt = cur.t0 + cur.count
-            if nxt < self.total:
-                self.fut = self.pool.submit(self._produce, self.slots[self.k % 2], nxt,
-                                            min(self.L, self.total - nxt))
+            if self.k + 2 < len(self.bounds) - 1:
+                self._submit(self.k + 2)
         i = t - cur.t0
         s = cur.slot
         return IterPlan(
@@ -235,8 +256,16 @@ class Lookahead:
                     self.tcp.gather_rows(bd[i], out=slot.RAg[i])
                 if r:
                     omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS
-                    K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
-                                  sketch[i], col_ids=bd[i])
+                    if self.sk_zop is not None:
+                        # K[B,B] Omega on the tensor cores: the block's own points
+                        # as columns, rows matched to columns by block position
+                        self.tcp.gather_cols(bd[i], out=self.sk_cols)
+                        self.sk_zop.fill(omc)
+                        K.krows_tc(self.o.spec, self.tcp, slot.RAg[i], b, self.sk_pos,
+                                   self.sk_zop, sketch[i], ws=self.sk_ws, cols=(self.sk_cols, 0))
+                    else:
+                        K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
+                                      sketch[i], col_ids=bd[i])
             if r:
                 Y = sketch.to(torch.float64)
                 omt = om.transpose(1, 2)

@@ -35,6 +35,7 @@ from __future__ import annotations
 
 import math
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -262,17 +263,35 @@ class SolverState:
     def iteration(self):
         return self._e.t
 
+    # widened to float64 and made row-major on the device, so the host gets one
+    # contiguous copy (no host-side conversion of an n x m array)
     @property
     def W(self):
-        return self._e.materialize("W").cpu().numpy().astype(np.float64)
+        return _to_host64(self._e.materialize("W"))
 
     @property
     def V(self):
-        return self._e.materialize("V").cpu().numpy().astype(np.float64)
+        return _to_host64(self._e.materialize("V"))
 
     @property
     def Z(self):
-        return self._e.materialize("Z").cpu().numpy().astype(np.float64)
+        return _to_host64(self._e.materialize("Z"))
+
+
+def _to_host64(t):
+    """Device tensor -> fresh C-contiguous float64 numpy array. The n x m copy
+    is bound by first-touch page faults of the new host array, so its pages
+    are faulted in by several threads before one device->host copy."""
+    src = t.to(torch.float64).contiguous()
+    out = np.empty(tuple(src.shape), dtype=np.float64)
+    flat = out.reshape(-1)
+    k = min(8, max(1, flat.size // (1 << 20)))
+    if k > 1:
+        with ThreadPoolExecutor(max_workers=k) as ex:
+            list(ex.map(lambda i: flat[i * flat.size // k:(i + 1) * flat.size // k].fill(0.0),
+                        range(k)))
+    torch.from_numpy(out).copy_(src)
+    return out
 
 
 class AdasapEngine:
@@ -526,7 +545,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
                 if averager is not None:
                     averager.add(done, W_loc)
                 if on_iterate is not None:
-                    on_iterate(done, eng.gather_full(W_loc).cpu().numpy().astype(np.float64))
+                    on_iterate(done, _to_host64(eng.gather_full(W_loc)))
             relres = math.nan
             if _due(config.residual_every, t, total):
                 W_loc = eng.materialize("W") if W_loc is None else W_loc
@@ -547,7 +566,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
             W_loc = averager.average()
         else:
             W_loc = eng.materialize("W")
-        W = eng.gather_full(W_loc).cpu().numpy().astype(np.float64)
+        W = _to_host64(eng.gather_full(W_loc))
     finally:
         eng.close()
     return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)

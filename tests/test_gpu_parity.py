@@ -189,3 +189,28 @@ def test_grad_at_w_and_tail_average_match_oracle_shape():
                         max_iters=6, tail_average=True, grad_eval_point="w")
     res = sap.adasap_solve(o, g["Y"], cfg)
     assert res.W.shape == g["Y"].shape and np.all(np.isfinite(res.W))
+
+
+@pytest.mark.parametrize("fam", ("rbf", "matern32"))
+def test_large_block_trajectory_tensor_core_sketch(fam):
+    """b >= 512 routes the Nystrom sketch K[B,B] Omega through the tensor-core
+    kernel (pipeline.py) and the block-row product through the CTA-pair
+    kernel: stepsizes and iterates against the oracle (solvers.py:361-403)."""
+    rng = np.random.default_rng(21)
+    n, d, b, r, m, iters = 6000, 5, 640, 60, 3, 6
+    X = rng.uniform(-2.0, 2.0, size=(n, d))
+    Y = rng.standard_normal((n, m))
+    ls = np.full(d, 1.3)
+    lam = 1e-2
+    pts = orc.Points(fam, ls, 1.0, X)
+    W_ref, eta_ref, crc_ref, _ = orc.adasap_solve(pts, lam, Y, iters, 7, b, r, workers=4)
+    o = sap.KernelOracle(sap.KernelSpec(fam, ls, 1.0), X, lam)
+    assert o.use_tc(r) and o.use_tc(m)
+    cfg = sap.RunConfig(lam=lam, blocksize=b, nystrom_rank=r, residual_every=0, seed=7,
+                        max_iters=iters)
+    res = sap.adasap_solve(o, Y, cfg)
+    crcs = np.array([rec.block_hash for rec in res.trace.records])
+    assert np.array_equal(crcs, crc_ref)
+    etas = np.array([rec.stepsize for rec in res.trace.records])
+    assert np.abs(etas - eta_ref).max() / np.abs(eta_ref).max() < 1e-4
+    assert rel(res.W, W_ref) < 1e-3
