@@ -50,7 +50,7 @@ METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--family", default=CONFIG["family"])
@@ -132,14 +132,24 @@ class ClockSampler:
         self.index = index
         self.proc = None
 
-    def start(self):
+    def start(self, settle_s=1.5):
+        """Start sampling and wait until nvidia-smi has settled (NVML start-up
+        contends with CUDA driver calls, so it must not overlap the timed
+        region's first launches); it keeps sampling through the region."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        t_end = time.time() + 5.0
+        while time.time() < t_end:
+            time.sleep(0.05)
+            if os.path.exists(self.path) and os.path.getsize(self.path) > 0:
+                break
+        time.sleep(max(0.0, settle_s - 0.0))
 
     def stop(self):
         if self.proc is None:
@@ -197,6 +207,8 @@ def run_b200(args):
     n_local = shard.size
     b, m, d = CONFIG["b"], CONFIG["m"], CONFIG["d"]
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         eng.step()
     torch.cuda.synchronize()
@@ -218,8 +230,6 @@ def run_b200(args):
 
     for name, fn in originals.items():
         setattr(S, name, timed(fn))
-    sampler = ClockSampler(local)
-    sampler.start()
     launches0 = lib.sap_launch_count()
     if dist:
         tdist.barrier()

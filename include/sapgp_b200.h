@@ -98,6 +98,27 @@ int sap_ktile(const float *Ra, const float *rasqn, const int64_t *row_ids, int64
               int ldx, int d, int family, double variance, double *out, int64_t ldo,
               void *stream);
 
+/* sap_ktile with fp32 output (the same fp32-computed values, half the bytes). */
+int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+                  const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc,
+                  int ldx, int d, int family, double variance, float *out, int64_t ldo,
+                  void *stream);
+
+/*
+ * Batched preconditioned power-iteration stepsize (replaces randnla.py:165-196
+ * rand_power_stepsize, called at solvers.py:389-396), for `count` independent
+ * problems q: H_q = P^{-1/2}(K_q + lam I)P^{-1/2} with
+ * P^{-1/2} x = x/sqrt(rho_q) + U_q diag(E_q) U_q^T x; `iters` steps from the
+ * unit vector v0_q; eta[q] = 1 / (v . H v) of the last step, bad[q] |= 1 when
+ * an iterate collapses or the estimate is not positive. K_q: fp32 [b][ldk] at
+ * Kbb + q*strideK; U_q: fp64 [b][r] at U + q*strideU; E: [count][r];
+ * rho, eta: [count]; v0: [count][b]. r may be 0 (U, E unused).
+ */
+int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK, const double *U,
+                       int64_t strideU, int r, const double *E, const double *rho,
+                       const double *v0, int b, int count, double lam, int iters, double *eta,
+                       int *bad, void *stream);
+
 /*
  * g[i, c] = G[i, c] + (own(i) ? lam * Z[j, c] - Y[j, c] : 0), j = loc[i],
  * Z = zp*P + zq*Q; rows with loc[i] < 0 belong to another shard.

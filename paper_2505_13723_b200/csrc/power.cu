@@ -1,0 +1,321 @@
+// Fused, batched power-iteration stepsize (reference randnla.py:165-196,
+// rand_power_stepsize, as called from solvers.py:389-396):
+//
+//   H = P^{-1/2} (K_BB + lam I) P^{-1/2},  P^{-1/2} x = x/sqrt(rho) + U diag(E) U^T x,
+//   E = (S + rho)^{-1/2} - rho^{-1/2},
+//   v <- v0;  10 x { y = H v;  est = v.y;  v = y/||y|| };  eta = 1/est.
+//
+// One thread-block cluster of kCluster CTAs per batch element (one ADASAP
+// iteration of a lookahead batch). CTA c of the cluster owns rows [lo, hi) of
+// K_BB (fp32, the values the tile kernel computes) and of U (fp64); the
+// length-b vector w = P^{-1/2} v is replicated in every CTA's shared memory
+// by DSMEM broadcast, and the three reductions of a step (U^T v, U^T z and
+// the two scalars v.y, |y|^2) combine per-CTA partials read over DSMEM in a
+// fixed rank order, so every CTA holds bitwise-identical results. K_BB is
+// streamed once per step (b^2 * 4 bytes): the kernel is bound by L2/HBM
+// bandwidth, replacing ~12 batched cuBLAS/elementwise launches per step.
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../include/sapgp_b200.h"
+
+namespace cg = cooperative_groups;
+
+namespace sap {
+
+int fail(int code, const char *fmt, ...);
+int check_launch(const char *what);
+
+namespace pw {
+
+constexpr int kCluster = 16;  // non-portable cluster size (B200 supports 16)
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRowsPerPass = 4;  // rows a warp dots at once (amortises w reads)
+
+struct Args {
+  const float *K;      // [count][b][ldk]
+  int64_t ldk, strideK;
+  const double *U;     // [count][b][r] (row-major) or null when r == 0
+  int64_t strideU;
+  const double *E;     // [count][r]
+  const double *rho;   // [count]
+  const double *v0;    // [count][b], unit norm
+  int b, r, iters;
+  double lam;
+  double *eta;         // [count]
+  int *bad;            // [count], OR-ed
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum of two values; result valid in every thread
+__device__ __forceinline__ void block_sum2(double &a, double &c, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  c = warp_sum(c);
+  __syncthreads();
+  if (lane == 0) {
+    red[2 * warp] = a;
+    red[2 * warp + 1] = c;
+  }
+  __syncthreads();
+  a = 0.0;
+  c = 0.0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    a += red[2 * w];
+    c += red[2 * w + 1];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const int u_smem) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const unsigned crank = cluster.block_rank();
+  const int q = blockIdx.x / kCluster;  // batch element
+  const int b = a.b, r = a.r;
+  const int per = (b + kCluster - 1) / kCluster;
+  const int lo = min(b, int(crank) * per), hi = min(b, lo + per);
+  const int nloc = hi - lo;
+  const int b4 = (b + 3) & ~3;
+
+  extern __shared__ __align__(16) double sm[];
+  double *vloc = sm;                  // [per]   v on own rows
+  double *zloc = vloc + per;          // [per]   w, then z, then y on own rows
+  double *part = zloc + per;          // [r]     own partial of U^T x
+  double *coef = part + r;            // [r]     E * (U^T x), full
+  double *spart = coef + r;           // [2]     own partial of v.y, |y|^2
+  double *red = spart + 2;            // [2*kWarps] block reduction scratch
+  double *scratch = red + 2 * kWarps; // [kThreads]
+  float *wf = reinterpret_cast<float *>(scratch + kThreads);  // [b4] replicated w (fp32)
+  double *us = reinterpret_cast<double *>(wf + b4);           // [nloc][r] own U rows (opt.)
+
+  const float *K = a.K + int64_t(q) * a.strideK;
+  const double *Ug = r ? a.U + int64_t(q) * a.strideU + int64_t(lo) * r : nullptr;
+  const double *E = r ? a.E + int64_t(q) * r : nullptr;
+  const double rho = a.rho[q];
+  const double isr = 1.0 / sqrt(rho);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool vec4 = (a.ldk & 3) == 0 && (a.strideK & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(a.K) & 15) == 0;
+  // own rows of U, from shared memory when they fit (loaded once)
+  const double *U = Ug;
+  if (u_smem && r) {
+    for (int e = tid; e < nloc * r; e += kThreads) us[e] = Ug[e];
+    U = us;
+  }
+  for (int i = tid; i < nloc; i += kThreads) vloc[i] = a.v0[int64_t(q) * b + lo + i];
+  for (int j = b + tid; j < b4; j += kThreads) wf[j] = 0.0f;
+  __syncthreads();
+
+  // coef = E * (U^T x) over the cluster, x given on own rows
+  auto ut_times = [&](const double *x) {
+    if (r <= kThreads) {
+      // kThreads / r row groups per column, combined in a fixed order
+      const int G = kThreads / r, g = tid / r, k = tid % r;
+      double s = 0.0;
+      if (g < G) {
+#pragma unroll 4
+        for (int i = g; i < nloc; i += G) s = fma(U[i * r + k], x[i], s);
+      }
+      scratch[tid] = s;
+      __syncthreads();
+      if (tid < r) {
+        double t = 0.0;
+        for (int gg = 0; gg < G; ++gg) t += scratch[gg * r + tid];
+        part[tid] = t;
+      }
+    } else {
+      for (int k = tid; k < r; k += kThreads) {
+        double t = 0.0;
+        for (int i = 0; i < nloc; ++i) t = fma(U[i * r + k], x[i], t);
+        part[k] = t;
+      }
+    }
+    cluster.sync();
+    for (int k = tid; k < r; k += kThreads) {
+      double v[kCluster];
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) v[c] = cluster.map_shared_rank(part, c)[k];
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < kCluster; ++c) s += v[c];
+      coef[k] = E[k] * s;
+    }
+    __syncthreads();
+  };
+  // out_i = x_i / sqrt(rho) + U[i,:] . coef on own rows: each thread owns rows
+  // tid, tid + kThreads, ... (U rows from shared memory; a thread's dot is
+  // sequential in k, the same order for every row)
+  auto apply_u = [&](const double *x, double *out) {
+    for (int i = tid; i < nloc; i += kThreads) {
+      double s = 0.0;
+      const double *ur = U + i * r;
+      for (int k = 0; k < r; ++k) s = fma(ur[k], coef[k], s);
+      out[i] = fma(x[i], isr, s);
+    }
+    __syncthreads();
+  };
+
+  double est = 0.0;
+  bool bad = false;
+#ifdef SAP_POWER_PROF
+  unsigned long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tc0 = clock64(), tc1;
+#define PP(k) do { tc1 = clock64(); tp[k] += tc1 - tc0; tc0 = tc1; } while (0)
+#else
+#define PP(k) do {} while (0)
+#endif
+  for (int it = 0; it < a.iters; ++it) {
+    // w = P^{-1/2} v on own rows -> broadcast (fp32) into every CTA's wf
+    if (r) ut_times(vloc);
+    PP(0);
+    apply_u(vloc, zloc);  // zloc holds w (own rows) for the moment
+    PP(1);
+    for (int c = 0; c < kCluster; ++c) {
+      float *dst = cluster.map_shared_rank(wf, c);
+      for (int i = tid; i < nloc; i += kThreads) dst[lo + i] = float(zloc[i]);
+    }
+    cluster.sync();
+    PP(2);
+    // z = K w + lam w on own rows: a warp dots kRowsPerPass rows at once, fp32
+    // products summed per lane (64 terms for b = 2000), lanes combined in fp64
+    for (int i0 = warp * kRowsPerPass; i0 < nloc; i0 += kWarps * kRowsPerPass) {
+      float acc[kRowsPerPass];
+#pragma unroll
+      for (int rr = 0; rr < kRowsPerPass; ++rr) acc[rr] = 0.0f;
+      if (vec4) {
+#pragma unroll 4
+        for (int j = lane * 4; j < b4; j += 128) {
+          const float4 w4 = *reinterpret_cast<const float4 *>(wf + j);
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerPass; ++rr) {
+            const int i = min(i0 + rr, nloc - 1);  // clamped rows are discarded below
+            const float4 kv = *reinterpret_cast<const float4 *>(K + int64_t(lo + i) * a.ldk + j);
+            acc[rr] = fmaf(kv.x, w4.x, acc[rr]);
+            acc[rr] = fmaf(kv.y, w4.y, acc[rr]);
+            acc[rr] = fmaf(kv.z, w4.z, acc[rr]);
+            acc[rr] = fmaf(kv.w, w4.w, acc[rr]);
+          }
+        }
+      } else {
+        for (int j = lane; j < b; j += 32) {
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerPass; ++rr) {
+            const int i = min(i0 + rr, nloc - 1);
+            acc[rr] = fmaf(K[int64_t(lo + i) * a.ldk + j], wf[j], acc[rr]);
+          }
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < kRowsPerPass; ++rr) {
+        const double s = warp_sum(double(acc[rr]));
+        const int i = i0 + rr;
+        if (lane == 0 && i < nloc) zloc[i] = fma(a.lam, zloc[i], s);
+      }
+    }
+    __syncthreads();
+    PP(3);
+    // y = P^{-1/2} z on own rows
+    if (r) ut_times(zloc);
+    PP(4);
+    double dvy = 0.0, dyy = 0.0;
+    for (int i = tid; i < nloc; i += kThreads) {
+      double s = 0.0;
+      const double *ur = U + i * r;
+      for (int k = 0; k < r; ++k) s = fma(ur[k], coef[k], s);
+      const double y = fma(zloc[i], isr, s);
+      dvy = fma(vloc[i], y, dvy);
+      dyy = fma(y, y, dyy);
+      zloc[i] = y;
+    }
+    PP(5);
+    block_sum2(dvy, dyy, red);
+    if (tid == 0) {
+      spart[0] = dvy;
+      spart[1] = dyy;
+    }
+    cluster.sync();
+    double sv[2 * kCluster];
+#pragma unroll
+    for (int c = 0; c < kCluster; ++c) {
+      const double *sp = cluster.map_shared_rank(spart, c);
+      sv[2 * c] = sp[0];
+      sv[2 * c + 1] = sp[1];
+    }
+    double vy = 0.0, yy = 0.0;
+#pragma unroll
+    for (int c = 0; c < kCluster; ++c) {
+      vy += sv[2 * c];
+      yy += sv[2 * c + 1];
+    }
+    est = vy;
+    const double ny = sqrt(yy);
+    bad = bad || ny == 0.0;
+    const double inv = ny > 0.0 ? 1.0 / ny : 0.0;
+    for (int i = tid; i < nloc; i += kThreads) vloc[i] = zloc[i] * inv;
+    PP(6);
+    // peers read this CTA's part/spart/wf only before the next cluster.sync
+    // of the following step, which every CTA reaches after these reads
+    __syncthreads();
+  }
+#ifdef SAP_POWER_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    printf("power prof (cycles): ut_v %llu apply_w %llu bcast+sync %llu gemv %llu ut_z %llu y %llu "
+           "red+sync %llu\n", tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp[6]);
+#endif
+  bad = bad || !(est > 0.0);
+  if (crank == 0 && tid == 0) {
+    a.eta[q] = 1.0 / est;
+    if (bad) a.bad[q] |= 1;
+  }
+  cluster.sync();  // no CTA exits while a peer may still read its shared memory
+}
+
+}  // namespace pw
+}  // namespace sap
+
+extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK,
+                                  const double *U, int64_t strideU, int r, const double *E,
+                                  const double *rho, const double *v0, int b, int count,
+                                  double lam, int iters, double *eta, int *bad, void *stream) {
+  using namespace sap;
+  if (b <= 0 || count <= 0 || iters <= 0 || r < 0 || ldk < b || (r && (!U || !E)))
+    return fail(SAP_ERR_CONTRACT, "power_stepsize: bad shape b=%d r=%d count=%d", b, r, count);
+  const int per = (b + pw::kCluster - 1) / pw::kCluster;
+  const size_t base = sizeof(double) * (2 * size_t(per) + 2 * size_t(r) + 2 + 2 * pw::kWarps +
+                                        pw::kThreads) +
+                      sizeof(float) * size_t((b + 3) & ~3);
+  const size_t with_u = base + sizeof(double) * size_t(per) * size_t(r);
+  constexpr size_t kCap = 200 * 1024;
+  if (base > kCap) return fail(SAP_ERR_CONTRACT, "power_stepsize: b=%d exceeds shared memory", b);
+  const int u_smem = with_u <= kCap ? 1 : 0;
+  const size_t smem = u_smem ? with_u : base;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pw::power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCap));
+    cudaFuncSetAttribute(pw::power_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  pw::Args a{Kbb, ldk, strideK, U, strideU, E, rho, v0, b, r, iters, lam, eta, bad};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(count * pw::kCluster));
+  cfg.blockDim = dim3(pw::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = pw::kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, pw::power_kernel, a, u_smem);
+  if (e != cudaSuccess) return fail(SAP_ERR_DEVICE, "power_kernel: %s", cudaGetErrorString(e));
+  return check_launch("power_kernel");
+}

@@ -70,11 +70,11 @@ __global__ void gather_points_kernel(const float *Xs, const float *sqn, int ldx,
 // result is bitwise symmetric: (rn_i + rn_j) - 2 sum_k a_k c_k is symmetric
 // term by term in IEEE arithmetic.
 
-template <int FAM>
+template <int FAM, typename T>
 __global__ void ktile_kernel(const float *Ra, const float *rasqn, const int64_t *row_ids,
                              int64_t na, const float *Rc, const float *rcsqn,
                              const int64_t *col_ids, int64_t nc, int ldx, int d, float variance,
-                             double *out, int64_t ldo) {
+                             T *out, int64_t ldo) {
   const int64_t i = int64_t(blockIdx.y) * blockDim.y + threadIdx.y;
   const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= na || j >= nc) return;
@@ -87,7 +87,7 @@ __global__ void ktile_kernel(const float *Ra, const float *rasqn, const int64_t 
     const float sq = fmaf(-2.0f, dot, rasqn[i] + rcsqn[j]);
     v = variance * kernel_value<FAM>(sq);
   }
-  out[i * ldo + j] = double(v);
+  out[i * ldo + j] = T(v);
 }
 
 // ---------------------------------------------------------------------------
@@ -219,6 +219,34 @@ int padded_dim(int ldx) {
 
 using namespace sap;
 
+template <typename T>
+static int ktile_launch(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+                        const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc,
+                        int ldx, int d, int family, double variance, T *out, int64_t ldo,
+                        void *stream) {
+  if (na <= 0 || nc <= 0 || ldo < nc || ldx < d || d < 1)
+    return fail(SAP_ERR_CONTRACT, "ktile: bad shape");
+  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 7) / 8));
+  cudaStream_t st = S(stream);
+  const float var = float(variance);
+  switch (family) {
+    case SAP_RBF:
+      ktile_kernel<SAP_RBF, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
+                                                     nc, ldx, d, var, out, ldo);
+      break;
+    case SAP_MATERN32:
+      ktile_kernel<SAP_MATERN32, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
+                                                          col_ids, nc, ldx, d, var, out, ldo);
+      break;
+    case SAP_MATERN52:
+      ktile_kernel<SAP_MATERN52, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
+                                                          col_ids, nc, ldx, d, var, out, ldo);
+      break;
+    default: return fail(SAP_ERR_CONTRACT, "ktile: unknown family %d", family);
+  }
+  return check_launch("ktile_kernel");
+}
+
 extern "C" {
 
 int sap_abi_version(void) { return SAP_ABI_VERSION; }
@@ -326,27 +354,16 @@ int sap_krows_times(const float *Xs, const float *sqn, int ldx, int64_t ncols,
 int sap_ktile(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
               const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc, int ldx,
               int d, int family, double variance, double *out, int64_t ldo, void *stream) {
-  if (na <= 0 || nc <= 0 || ldo < nc || ldx < d || d < 1)
-    return fail(SAP_ERR_CONTRACT, "ktile: bad shape");
-  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 7) / 8));
-  cudaStream_t st = S(stream);
-  const float var = float(variance);
-  switch (family) {
-    case SAP_RBF:
-      ktile_kernel<SAP_RBF><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids, nc,
-                                                  ldx, d, var, out, ldo);
-      break;
-    case SAP_MATERN32:
-      ktile_kernel<SAP_MATERN32><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
-                                                       nc, ldx, d, var, out, ldo);
-      break;
-    case SAP_MATERN52:
-      ktile_kernel<SAP_MATERN52><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
-                                                       nc, ldx, d, var, out, ldo);
-      break;
-    default: return fail(SAP_ERR_CONTRACT, "ktile: unknown family %d", family);
-  }
-  return check_launch("ktile_kernel");
+  return ktile_launch(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids, nc, ldx, d, family, variance,
+                      out, ldo, stream);
+}
+
+int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+                  const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc,
+                  int ldx, int d, int family, double variance, float *out, int64_t ldo,
+                  void *stream) {
+  return ktile_launch(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids, nc, ldx, d, family, variance,
+                      out, ldo, stream);
 }
 
 int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q, const float *Y,

@@ -222,6 +222,25 @@ def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False, co
     return out
 
 
+def ktile_f32(spec, A, asq, aid, C, csq, cid, ldx, d, out):
+    """fp32 K(A, C) into ``out`` (same values as ktile, half the bytes)."""
+    nat.call("sap_ktile_f32", nat.ptr(A), nat.ptr(asq), nat.ptr(aid), A.shape[0], nat.ptr(C),
+             nat.ptr(csq), nat.ptr(cid), C.shape[0], ldx, d, spec.code, spec.variance,
+             nat.ptr(out), out.stride(0), nat.stream_handle())
+    return out
+
+
+def power_stepsize(Kbb, U, E, rho, v0, lam, iters, eta, bad):
+    """Batched preconditioned power iteration (randnla.py:165-196) over the
+    leading ``Kbb.shape[0]`` problems: eta[q] = 1/(v.Hv), bad[q] |= failure."""
+    count, b = Kbb.shape[0], Kbb.shape[1]
+    r = 0 if U is None else U.shape[2]
+    nat.call("sap_power_stepsize", nat.ptr(Kbb), Kbb.stride(1), Kbb.stride(0),
+             nat.ptr(U) if r else None, U.stride(0) if r else 0, r, nat.ptr(E) if r else None,
+             nat.ptr(rho), nat.ptr(v0), b, count, lam, iters, nat.ptr(eta), nat.ptr(bad),
+             nat.stream_handle())
+
+
 def ktile(spec, A, asq, aid, C, csq, cid, ldx, d):
     out = torch.empty((A.shape[0], C.shape[0]), dtype=torch.float64, device=A.device)
     nat.call("sap_ktile", nat.ptr(A), nat.ptr(asq), nat.ptr(aid), A.shape[0], nat.ptr(C),

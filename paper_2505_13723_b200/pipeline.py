@@ -11,8 +11,9 @@ block-row product and the update depends only on (seed, t) and X:
     eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
                                    10, substream(seed, "power", t)) :389-396
 
-so they are produced in batches on a side CUDA stream and a host worker
-thread, up to two batches ahead of the main stream's block-row products.
+so they are produced in batches by two host producer threads, up to two
+batches ahead of the block-row products that consume them; their GPU work is
+enqueued in order on the solver's stream (see Lookahead.__init__).
 Batch sizes ramp 1, 2, 4, ... up to ``L = config.lookahead`` so the first
 iteration waits for one plan only, not for a full batch. Per batch there is one device->host
 round trip (three r x r matrices per iteration) for the host LAPACK part
@@ -26,6 +27,7 @@ from __future__ import annotations
 
 import math
 import os
+import sys
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -68,8 +70,9 @@ class _Slot:
         self.E = torch.zeros((L, max(r, 1)), dtype=f64, device=dev)
         self.rho = torch.ones(L, dtype=f64, device=dev)
         self.v0 = torch.empty((L, b), dtype=f64, device=dev)
-        self.Kbb = torch.empty((L, b, b), dtype=f64, device=dev)
-        self.graph = None  # CUDA graph of the batched power iteration (full batches)
+        # K_BB in fp32: the values the tile kernel computes (fp32 arithmetic),
+        # streamed once per power step by sap_power_stepsize
+        self.Kbb = torch.empty((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
         bpad = (b + 255) // 256 * 256
@@ -105,35 +108,48 @@ class Lookahead:
                  tcp=None):
         self.o, self.shard, self.seed = oracle, shard, seed
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
-        # three slots of L fp64 b x b blocks: keep them under ~3 GB
-        cap = max(1, int(3e9 // (3 * 8 * b * b)))
+        # three slots of L fp32 b x b blocks: keep them under ~3 GB
+        cap = max(1, int(3e9 // (3 * 4 * b * b)))
         self.total, self.L = total, max(1, min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
         self.dev = dev
-        # high priority: the side chain's short kernels run in the gaps between the
-        # persistent block-row kernels instead of queueing behind the next one
-        self.side = torch.cuda.Stream(device=dev, priority=-1)
+        # Production is enqueued in order on the solver's stream. The block-row
+        # kernel is persistent (one CTA per SM, registers and shared memory
+        # full), so nothing co-runs with it: a side-stream kernel that takes
+        # the SMs a draining block-row kernel frees holds the next one back
+        # (measured, config 3 on one B200: 380-430 iters/s with per-slot
+        # high-priority side streams, krows up to 2.6 ms; 470-520 in order).
+        # SAP_SIDE_STREAM=1 selects the side streams for experiments.
+        if os.environ.get("SAP_SIDE_STREAM", "0") == "1":
+            self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(3)]
+        else:
+            self.sides = [torch.cuda.current_stream(dev)] * 3
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
         self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(3)]
-        # side-stream scratch of the tensor-core sketch (used one plan at a time)
+        # per-slot scratch of the tensor-core sketch (used one plan at a time by
+        # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
         # mostly padding and the FFMA sketch, ~4x more precise, costs little)
-        self.sk_zop = None
-        if tcp is not None and self.r and b >= 512 and oracle.use_tc(self.r):
-            self.sk_zop = K.ZOperand(self.r, b, dev)
-            self.sk_cols = torch.empty((b, ka), dtype=torch.float32, device=dev)
+        self.tc_sketch = tcp is not None and self.r and b >= 512 and oracle.use_tc(self.r)
+        if self.tc_sketch:
             self.sk_pos = torch.arange(b, dtype=torch.int64, device=dev)
             need = K.nat.load().sap_krows_tc_workspace(b, self.r, b)
-            self.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
+            for slot in self.slots:
+                slot.sk_zop = K.ZOperand(self.r, b, dev)
+                slot.sk_cols = torch.empty((b, ka), dtype=torch.float32, device=dev)
+                slot.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
         # batch k covers iterations [bounds[k], bounds[k+1])
         self.bounds = [0]
         c = 1
         while self.bounds[-1] < total:
             self.bounds.append(min(total, self.bounds[-1] + c))
             c = min(2 * c, self.L)
-        self.pool = ThreadPoolExecutor(max_workers=1, thread_name_prefix="sap-lookahead")
+        # two producers: a batch's production (host RNG -> sketch on the GPU ->
+        # host factorisation -> power iteration) takes longer than consuming
+        # one, so two batches are produced concurrently (slots k, k+1 mod 3)
+        self.pool = ThreadPoolExecutor(max_workers=2, thread_name_prefix="sap-lookahead")
         # host workers for the per-iteration numpy RNG and r x r LAPACK work (both
         # release the GIL in their kernels); sized to leave cores for the main thread
         try:
@@ -143,6 +159,13 @@ class Lookahead:
         self.hostpool = ThreadPoolExecutor(max_workers=max(1, min(self.L, cores - 2, 8)),
                                            thread_name_prefix="sap-host")
         self.timings = [] if os.environ.get("SAP_PROFILE") else None
+        # The solver thread enqueues ~20 launches per iteration and must keep
+        # ahead of the device while the producer and host workers run Python
+        # between their numpy/LAPACK calls: with CPython's default 5 ms GIL
+        # switch interval it can wait a whole interval for the GIL, longer than
+        # an iteration's device time. 0.2 ms bounds that wait.
+        if sys.getswitchinterval() > 2e-4:
+            sys.setswitchinterval(2e-4)
         # r x r LAPACK calls from several host workers: one BLAS thread each (the
         # reference pins BLAS to one thread for the same reason, __init__.py:16-22)
         try:
@@ -152,26 +175,14 @@ class Lookahead:
             self._blas_limit = None
         self.cur = None
         self.k = -1  # batch currently consumed
-        # capture both slots' power-iteration graphs up front (static buffers; the
-        # values are filled per batch), so no capture lands inside a timed solve
-        if self.L > 1:
-            with torch.cuda.device(dev), torch.cuda.stream(self.side):
-                for slot in self.slots:
-                    slot.v0.fill_(1.0)
-                    slot.Kbb.zero_()
-                    self._power(slot, self.L)  # warm-up (allocator, cuBLAS handles)
-                    slot.graph = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(slot.graph, stream=self.side,
-                                          capture_error_mode="thread_local"):
-                        self._power(slot, self.L)
-                    slot.bad.zero_()
         self.futs = {}
         for k in range(min(2, len(self.bounds) - 1)):
             self._submit(k)
 
     def _submit(self, k):
         t0, t1 = self.bounds[k], self.bounds[k + 1]
-        self.futs[k] = self.pool.submit(self._produce, self.slots[k % 3], t0, t1 - t0)
+        self.futs[k] = self.pool.submit(self._produce, self.slots[k % 3], t0, t1 - t0,
+                                        self.sides[k % 3])
 
     def close(self):
         self.pool.shutdown(wait=True)
@@ -212,7 +223,7 @@ class Lookahead:
                                      "estimate; H is not PSD)")
 
     # -- producer side (worker thread) ------------------------------------------
-    def _produce(self, slot, t0, count):
+    def _produce(self, slot, t0, count, side):
         b, r, seed, n = self.b, self.r, self.seed, self.n
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
@@ -239,7 +250,6 @@ class Lookahead:
         blocks = [d[0] for d in drawn]
         crcs = [d[1] for d in drawn]
         tm1 = time.perf_counter()
-        side = self.side
         pts = self.o.points
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
             if slot.free is not None:
@@ -256,13 +266,14 @@ class Lookahead:
                     self.tcp.gather_rows(bd[i], out=slot.RAg[i])
                 if r:
                     omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS
-                    if self.sk_zop is not None:
+                    if self.tc_sketch:
                         # K[B,B] Omega on the tensor cores: the block's own points
                         # as columns, rows matched to columns by block position
-                        self.tcp.gather_cols(bd[i], out=self.sk_cols)
-                        self.sk_zop.fill(omc)
+                        self.tcp.gather_cols(bd[i], out=slot.sk_cols)
+                        slot.sk_zop.fill(omc)
                         K.krows_tc(self.o.spec, self.tcp, slot.RAg[i], b, self.sk_pos,
-                                   self.sk_zop, sketch[i], ws=self.sk_ws, cols=(self.sk_cols, 0))
+                                   slot.sk_zop, sketch[i], ws=slot.sk_ws,
+                                   cols=(slot.sk_cols, 0))
                     else:
                         K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
                                       sketch[i], col_ids=bd[i])
@@ -303,54 +314,32 @@ class Lookahead:
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
             for i in range(count):
                 Xb, rsq = slot.Xb[i], slot.rsq[i]
-                slot.Kbb[i] = K.ktile(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d)
+                K.ktile_f32(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d,
+                            slot.Kbb[i])
             slot.rho[:count].copy_(slot.h_rho[:count], non_blocking=True)
             if r:
                 w = slot.h_w[:count].to(self.dev, non_blocking=True)
                 torch.bmm(Y, w[:, 0], out=slot.U[:count])
                 slot.Mc[:count].copy_(w[:, 1])
                 slot.E[:count].copy_(slot.h_coef[:count], non_blocking=True)
-            if count == self.L and slot.graph is not None:
-                slot.graph.replay()
-            else:
-                self._power(slot, count)
+            inputs = torch.cuda.Event()
+            inputs.record(side)
+        # The power iteration is one long cluster kernel on 128 SMs: on the side
+        # stream it would take the SMs a draining block-row kernel frees and hold
+        # the next one back for its whole duration, so it is enqueued on the
+        # solver's stream, between two block-row products.
+        with torch.cuda.device(self.dev), torch.cuda.stream(self.main):
+            self.main.wait_event(inputs)
+            K.power_stepsize(slot.Kbb[:count], slot.U[:count] if r else None,
+                             slot.E[:count], slot.rho[:count], slot.v0[:count], self.lam,
+                             self.iters, slot.eta[:count], slot.bad[:count])
             ready = torch.cuda.Event()
-            ready.record(side)
+            ready.record(self.main)
             slot.h2d_done = ready  # pinned host buffers reusable after this point
         if self.timings is not None:
             self.timings.append(dict(count=count, rng=tm1 - tm0, gpu_wait=tm2 - tm1,
                                      factor=tm3 - tm2, total=time.perf_counter() - tm0))
         return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready)
-
-    def _power(self, slot, count):
-        """Batched rand_power_stepsize (randnla.py:165-196) on P^{-1/2}(K+lam)P^{-1/2},
-        P^{-1/2} x = x/sqrt(rho) + U diag((S+rho)^{-1/2} - rho^{-1/2}) U^T x,
-        from the slot's static buffers (so full batches replay as one CUDA graph)."""
-        Kbb, v, U, E = slot.Kbb[:count], slot.v0[:count], None, slot.E[:count]
-        if self.r:
-            U = slot.U[:count]
-        isr = slot.rho[:count].rsqrt()[:, None]
-
-        def pinv_sqrt(x):
-            y = x * isr
-            if U is not None:
-                y = y + torch.bmm(U, (E * torch.bmm(U.transpose(1, 2), x[:, :, None])[:, :, 0])
-                                  [:, :, None])[:, :, 0]
-            return y
-
-        bad = torch.zeros(count, dtype=torch.bool, device=self.dev)
-        est = None
-        for _ in range(self.iters):
-            w = pinv_sqrt(v)
-            z = torch.bmm(Kbb, w[:, :, None])[:, :, 0] + self.lam * w
-            y = pinv_sqrt(z)
-            est = (v * y).sum(dim=1)
-            ny = torch.linalg.vector_norm(y, dim=1)
-            bad |= ny == 0
-            v = y / ny[:, None]
-        bad |= est <= 0
-        slot.eta[:count].copy_(1.0 / est)
-        slot.bad[:count].bitwise_or_(bad.to(torch.int32))
 
 
 class _Cols:

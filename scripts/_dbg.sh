@@ -1,1 +1,1 @@
-for v in variants/*.so; do echo "== $v"; SAP_LIB_PATH=$PWD/$v timeout 100 python scripts/tc_check.py 2>&1 | grep -E "tc-vs-oracle|tc vs"; for fam in rbf matern32; do SAP_LIB_PATH=$PWD/$v timeout 60 python scripts/krows_once.py --reps 5 --family $fam; done; done
+timeout 120 python scripts/timeline.py; SAP_SIDE_STREAM=1 timeout 120 python scripts/timeline.py

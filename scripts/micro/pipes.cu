@@ -8,6 +8,8 @@ template <int OP>
 __global__ void probe(float *out, int iters, unsigned long long *cyc) {
   float v[8];
   uint32_t u[8];
+  double dv[8];
+  for (int i = 0; i < 8; ++i) dv[i] = 0.5 + threadIdx.x * 1e-3 + i;
   for (int i = 0; i < 8; ++i) { v[i] = 0.001f * (threadIdx.x + i); u[i] = threadIdx.x * 7 + i; }
   __syncthreads();
   unsigned long long c0 = clock64();
@@ -27,11 +29,14 @@ __global__ void probe(float *out, int iters, unsigned long long *cyc) {
       if constexpr (OP == 10) { asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u[i])); }
       if constexpr (OP == 11) { asm volatile("tanh.approx.f32 %0, %0;" : "+f"(v[i])); }
       if constexpr (OP == 12) { asm volatile("sqrt.approx.ftz.f32 %0, %0;" : "+f"(v[i])); }
+      if constexpr (OP == 13) { double dd = v[i]; asm volatile("fma.rn.f64 %0, %0, 0d3FF0000000000001, 0d3FE0000000000000;" : "+d"(dd)); v[i] = float(dd); }
+      if constexpr (OP == 15) { asm volatile("fma.rn.f64 %0, %0, 0d3FF0000000000001, 0d3FE0000000000000;" : "+d"(dv[i])); }
+      if constexpr (OP == 14) { double dd; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(dd) : "f"(v[i])); asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(v[i]) : "d"(dd)); }
     }
   }
   unsigned long long c1 = clock64();
   float s = 0;
-  for (int i = 0; i < 8; ++i) s += v[i] + __uint_as_float(u[i]);
+  for (int i = 0; i < 8; ++i) s += v[i] + __uint_as_float(u[i]) + float(dv[i]);
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
   if (threadIdx.x == 0) cyc[blockIdx.x] = c1 - c0;
 }
@@ -41,12 +46,12 @@ int main() {
   const int warps = 16, iters = 4096, blocks = 148;
   cudaMalloc(&out, blocks * warps * 32 * 4);
   cudaMalloc(&cyc, blocks * 8);
-  const char *names[] = {"ex2.ftz", "rsqrt", "cvt.f16x2.f32", "cvt.f32.f16", "fadd", "fmax", "ex2+fadd", "ex2+cvtpack", "ffma", "ex2(noftz)", "ex2.bf16x2", "tanh", "sqrt"};
-  for (int op = 0; op < 13; ++op) {
+  const char *names[] = {"ex2.ftz", "rsqrt", "cvt.f16x2.f32", "cvt.f32.f16", "fadd", "fmax", "ex2+fadd", "ex2+cvtpack", "ffma", "ex2(noftz)", "ex2.bf16x2", "tanh", "sqrt", "dfma(+2cvt)", "cvt f32<->f64", "dfma"};
+  for (int op = 13; op < 16; ++op) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (op) {
 #define L(K) case K: probe<K><<<blocks, warps * 32>>>(out, iters, cyc); break;
-        L(0) L(1) L(2) L(3) L(4) L(5) L(6) L(7) L(8) L(9) L(10) L(11) L(12)
+        L(0) L(1) L(2) L(3) L(4) L(5) L(6) L(7) L(8) L(9) L(10) L(11) L(12) L(13) L(14) L(15)
       }
     }
     cudaDeviceSynchronize();

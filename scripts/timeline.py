@@ -1,0 +1,47 @@
+"""Kernel timeline of steady-state ADASAP iterations (torch.profiler / CUPTI):
+device busy fraction, idle gaps and what precedes/follows them."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from torch.profiler import profile, ProfilerActivity
+import paper_2505_13723_b200 as sap
+from paper_2505_13723_b200 import synthetic
+from paper_2505_13723_b200.solvers import AdasapEngine
+n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
+prob = synthetic.make_problem(n, d, "matern32", m, seed=0, lam=1e-2, device="cuda", rhs="noise")
+o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
+cfg = sap.RunConfig(lam=prob.lam, blocksize=b, nystrom_rank=r, residual_every=0, max_iters=80)
+eng = AdasapEngine(o, prob.Y, cfg, sap.resolve_accel(cfg, n, b), total=80)
+for _ in range(16): eng.step()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(24): eng.step()
+    torch.cuda.synchronize()
+eng.close()
+path = "/tmp/trace.json"
+prof.export_chrome_trace(path)
+ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
+ev.sort(key=lambda e: e["ts"])
+t0, t1 = ev[0]["ts"], max(e["ts"] + e["dur"] for e in ev)
+busy, cur_end, gaps = 0.0, t0, []
+for i, e in enumerate(ev):
+    s, f = e["ts"], e["ts"] + e["dur"]
+    if s > cur_end:
+        gaps.append((s - cur_end, ev[i - 1]["name"][:50] if i else "", e["name"][:50]))
+    busy += max(0.0, f - max(s, cur_end))
+    cur_end = max(cur_end, f)
+span = t1 - t0
+print(f"span {span/24:.1f} us/iter, busy {busy/24:.1f} us/iter ({100*busy/span:.1f}%), kernels {len(ev)}")
+gaps.sort(reverse=True)
+tot = sum(g[0] for g in gaps)
+print(f"idle {tot/24:.1f} us/iter in {len(gaps)} gaps; largest:")
+for g in gaps[:15]:
+    print(f"  {g[0]:8.1f} us  after {g[1]!r}  before {g[2]!r}")
+streams = {}
+for e in ev:
+    streams.setdefault(e["args"].get("stream"), []).append(e)
+for sid, es in streams.items():
+    print(f"stream {sid}: {len(es)} kernels, {sum(e['dur'] for e in es)/24:.1f} us/iter")
+# krows kernels: duration stats
+kr = [e["dur"] for e in ev if "krows_tc2_kernel<1, 80" in e["name"]]
+print("krows us:", [round(x) for x in kr[:24]])
