@@ -121,6 +121,7 @@ class Lookahead:
         # (measured, config 3 on one B200: 380-430 iters/s with per-slot
         # high-priority side streams, krows up to 2.6 ms; 470-520 in order).
         # SAP_SIDE_STREAM=1 selects the side streams for experiments.
+        self.main = torch.cuda.current_stream(dev)
         if os.environ.get("SAP_SIDE_STREAM", "0") == "1":
             self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(3)]
         else:
