@@ -41,7 +41,7 @@ for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at this
 # config, from the committed ncu capture (profiles/); re-capture when the kernel changes.
-TRAFFIC_PER_LAUNCH = 505_737_728  # profiles/r01_krows_tc_m32_ncu_summary.txt (486.38 MB read + 19.36 MB write)
+TRAFFIC_PER_LAUNCH = 508_532_736  # profiles/r01_krows_tc2_m32_ncu_summary.txt (488.02 MB read + 20.51 MB write)
 
 CONFIG = dict(n=1_000_000, d=9, family="matern32", b=2000, m=65, r=100, lam=1e-2, seed=0)
 METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target RMSE"
@@ -284,6 +284,20 @@ def run_b200(args):
         pass
 
     bf16_peak = float(peaks.get("bf16_tflops", 1590.0))
+    # What the tensor pipe must execute per kernel entry in this formulation
+    # (DESIGN.md §5): GEMM1 kind::tf32 over the ka augmented features, GEMM2
+    # kind::f16 three split passes over nz padded right-hand sides. tf32 dense
+    # peak taken as half the measured bf16 peak (no tf32 figure is measured).
+    tensor_pipe = None
+    if eng.use_tc:
+        ka, nz = eng.tcp.ka, eng.zop.nz
+        t_entry = 2 * ka / (0.5 * bf16_peak * 1e12) + 3 * 2 * nz / (bf16_peak * 1e12)
+        ideal_ms = b * n_local * t_entry * 1e3
+        tensor_pipe = {"hw_flop_per_entry": {"tf32": 2 * ka, "f16": 6 * nz},
+                       "ideal_ms_at_peak": ideal_ms, "frac": ideal_ms / kmean,
+                       "note": "time the tensor pipe needs for GEMM1 (tf32, ka=%d) + GEMM2 (3 "
+                               "fp16 passes, nz=%d) at the measured bf16 peak (tf32 = half) "
+                               "over the measured kernel time" % (ka, nz)}
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, prob, spec, dev)
@@ -311,7 +325,8 @@ def run_b200(args):
                      "algorithmic": f"{b}*{n_local}*2*({d}+{m}) flop per launch "
                                     "(2d+2m per kernel entry, BASELINE.md §2)",
                      "fp32_ffma_peak": ffma_peak,
-                     "frac_of_fp32_ffma_roofline": achieved / ffma_peak},
+                     "frac_of_fp32_ffma_roofline": achieved / ffma_peak,
+                     "tensor_pipe": tensor_pipe},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
