@@ -70,10 +70,10 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 
 // which of the 32 entries of a TMEM chunk take the polynomial exp2 (measured
-// sweep, config 3: RBF 1/8 of the entries -2%; Matern none -- the epilogue is
-// issue/latency-bound there, not MUFU-bound)
+// sweeps, config 3, after the epilogue's clock instrumentation was compiled
+// out: none for either family -- RBF 1/8 +2.4%, 1/4 +3.3%; Matern 1/8 +3.7%)
 #ifndef SAP_POLY_RBF_MASK
-#define SAP_POLY_RBF_MASK 0x80808080u
+#define SAP_POLY_RBF_MASK 0x0u
 #endif
 #ifndef SAP_POLY_MAT_MASK
 #define SAP_POLY_MAT_MASK 0x0u

@@ -19,6 +19,15 @@
 
 #include "krows_tc.cuh"
 
+#ifndef SAP_EPI_PIPE
+#define SAP_EPI_PIPE 0
+#endif
+// per-role cycle timers (SAP_TC_PROF=1 at run time needs a -DSAP_TC_TIMERS=1
+// build); compiled out otherwise -- the clock reads cost epilogue issue slots
+#ifndef SAP_TC_TIMERS
+#define SAP_TC_TIMERS 0
+#endif
+
 namespace sap {
 namespace tck2 {
 
@@ -31,6 +40,25 @@ using tck::pvalue;
 using tck::split2;
 using tck::split_range;
 using tck::kDescBase;
+
+#ifndef SAP_EPI_SPIN
+#define SAP_EPI_SPIN 0
+#endif
+__device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity) {
+#if SAP_EPI_SPIN
+  tc::mbar_wait_spin(bar, parity);
+#else
+  tc::mbar_wait(bar, parity);
+#endif
+}
+
+__device__ __forceinline__ unsigned long long prof_clock() {
+#if SAP_TC_TIMERS
+  return clock64();
+#else
+  return 0ull;
+#endif
+}
 
 constexpr int NT = 128;     // points per column tile (64 staged per CTA)
 constexpr int NB = 3;       // S/P tiles in flight in TMEM (columns 0..383)
@@ -76,7 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t cr = tc::cluster_ctarank();   // 0 = leader (issues the MMAs)
-  const unsigned long long kstart = clock64();
+  const unsigned long long kstart = prof_clock();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   uint8_t *sA = smem;                          // [2][a_bytes]
@@ -148,9 +176,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc::tma_load_2d_pair(tc::smem_u32(sA + ab * Geo::a_bytes + ka * BM * 128), &tm_rows,
                                abar, ka * 32, rt * 2 * BM + int(cr) * BM);
         for (int64_t t = t0; t < t1; ++t) {
-          c0 = clock64();
+          c0 = prof_clock();
           tc::mbar_wait(empty0 + 8 * s, ph ^ 1);
-          const unsigned long long c1 = clock64();
+          const unsigned long long c1 = prof_clock();
           tw += c1 - c0;
           const uint32_t fbar = full0 + 8 * s;
           if (cr == 0) tc::mbar_expect_tx(fbar, 2 * Geo::stage_bytes);
@@ -167,7 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc::tma_load_2d_pair(st + Geo::x_bytes + Geo::z_bytes + za * Geo::z_atom, &tm_zlo,
                                  fbar, col0 + za * 64, int(cr) * (NZ / 2));
           }
-          ti += clock64() - c1;
+          ti += prof_clock() - c1;
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -201,10 +229,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t a_desc = a_desc0 + ((ab * Geo::a_bytes) >> 4);
         int g1 = 0;  // GEMM1s issued in this unit
         auto gemm1 = [&]() {
-          cc = clock64();
+          cc = prof_clock();
           tc::mbar_wait(full0 + 8 * s1, ph1);
           tc::fence_after();
-          const unsigned long long cw = clock64();
+          const unsigned long long cw = prof_clock();
           wf += cw - cc;
           const uint64_t x_desc = stage_desc0 + ((s1 * Geo::stage_bytes) >> 4);
           const uint32_t d = tmem + r1 * NT;
@@ -215,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc::mma_tf32_ss_pair(d, a_desc + ko, x_desc + kx, id1, k > 0);
           }
           tc::commit_pair(sfull0 + 8 * r1);
-          i1 += clock64() - cw;
+          i1 += prof_clock() - cw;
           if (++s1 == STAGES) { s1 = 0; ph1 ^= 1; }
           if (++r1 == NB) r1 = 0;
           if (++g1 == nt) tc::commit_pair(tc::smem_u32(&a_empty[ab]));
@@ -229,13 +257,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           while (g1 < nt && g1 <= j + NB - 1) gemm1();
           const bool seg_first = seg_j == 0;
           const bool seg_last = seg_j == kSeg - 1 || j + 1 == nt;
-          cc = clock64();
+          cc = prof_clock();
           if (seg_first) tc::mbar_wait_cluster(tc::smem_u32(g_empty), (sc & 1) ^ 1);
-          const unsigned long long cg = clock64();
+          const unsigned long long cg = prof_clock();
           wg += cg - cc;
           tc::mbar_wait_cluster(pfull0 + 8 * r2, ph2);
           tc::fence_after();
-          const unsigned long long cp = clock64();
+          const unsigned long long cp = prof_clock();
           wp += cp - cg;
           const uint64_t zhi = stage_desc0 + ((s2 * Geo::stage_bytes + Geo::x_bytes) >> 4);
           const uint64_t zlo = zhi + (Geo::z_bytes >> 4);
@@ -259,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           } else {
             ++seg_j;
           }
-          i2 += clock64() - cp;
+          i2 += prof_clock() - cp;
           if (++s2 == STAGES) s2 = 0;
           if (++r2 == NB) { r2 = 0; ph2 ^= 1; }
         }
@@ -297,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float *pend_dst = nullptr;
     unsigned long long es = 0, ec = 0, ed = 0, ea = 0, ce;
     auto drain = [&]() {  // add a finished TMEM segment, one tile late
-      tc::mbar_wait(tc::smem_u32(g_full), sc & 1);
+      epi_wait(tc::smem_u32(g_full), sc & 1);
       tc::fence_after();
       const uint32_t gbase = tmem + lane_off + kGCol;
 #pragma unroll
@@ -329,6 +357,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
       }
     };
+#if SAP_EPI_PIPE
+    // P for 16 of this warp's 32 tile columns (entries e0..e0+15): o[0..7] the
+    // packed fp16 hi words, o[8..15] the lo words
+    auto convert16 = [&](const uint32_t(&v)[16], int e0, int dc, bool diag, uint32_t(&o)[16]) {
+      if (p.debug == 1) {  // profiling: tensor/TMEM pipeline without the epilogue math
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = v[e];
+      } else if (p.debug == 11) {  // profiling: split only, kernel value -> one FMUL
+#pragma unroll
+        for (int e = 0; e < 16; e += 2)
+          split2(__uint_as_float(v[e]) * 1.5f, __uint_as_float(v[e + 1]) * 1.5f, o[e / 2], o[8 + e / 2]);
+      } else if (p.debug == 12) {  // profiling: kernel value only, no fp16 split
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          o[e / 2] = __float_as_uint(pvalue<FAM>(__uint_as_float(v[e])));
+          o[8 + e / 2] = __float_as_uint(pvalue<FAM>(__uint_as_float(v[e + 1])));
+        }
+      } else if (p.debug == 13) {  // profiling: FMA-pipe exp2 everywhere
+#pragma unroll
+        for (int e = 0; e < 16; e += 2)
+          split2(pvalue<FAM, true>(__uint_as_float(v[e])), pvalue<FAM, true>(__uint_as_float(v[e + 1])),
+                 o[e / 2], o[8 + e / 2]);
+      } else if (__any_sync(0xffffffffu, diag)) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          float p0 = pvalue<FAM>(__uint_as_float(v[e]));
+          float p1 = pvalue<FAM>(__uint_as_float(v[e + 1]));
+          if (diag && dc == e0 + e) p0 = kPScale;
+          if (diag && dc == e0 + e + 1) p1 = kPScale;
+          split2(p0, p1, o[e / 2], o[8 + e / 2]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const float x0 = __uint_as_float(v[e]), x1 = __uint_as_float(v[e + 1]);
+          split2(poly_entry<FAM>(e0 + e) ? pvalue<FAM, true>(x0) : pvalue<FAM>(x0),
+                 poly_entry<FAM>(e0 + e + 1) ? pvalue<FAM, true>(x1) : pvalue<FAM>(x1),
+                 o[e / 2], o[8 + e / 2]);
+        }
+      }
+    };
+#endif
     for (int u = pair; u < units; u += npairs) {
       const int rt = u % p.row_tiles, split = u / p.row_tiles;
       int64_t t0, t1;
@@ -345,11 +415,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
       }
       int seg_j = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        ce = clock64();
-        tc::mbar_wait(sfull0 + 8 * r, ph);
+#if SAP_EPI_PIPE
+      // Software-pipelined conversion in 16-column chunks: the TMEM load of the
+      // next chunk (the next tile's first chunk across the tile boundary) is in
+      // flight while this chunk's MUFU work runs, so the four warps sharing a
+      // sub-partition keep the MUFU pipe fed instead of all stalling on tile
+      // loads and stores at the same time.
+      uint32_t va[16], vb[16], oa[16], ob[16];
+      if (t0 < t1) {
+        epi_wait(sfull0 + 8 * r, ph);
         tc::fence_after();
-        const unsigned long long cs = clock64();
+        tc::ld16(tmem + lane_off + r * NT + w * 32, va);
+        tc::wait_ld();
+      }
+      for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t taddr = tmem + lane_off + r * NT + w * 32;
+        tc::ld16(taddr + 16, vb);
+        const int64_t dc64 = rid - (p.col_base + t * NT) - w * 32;
+        const bool diag = dc64 >= 0 && dc64 < 32;
+        const int dc = int(dc64);
+        convert16(va, 0, dc, diag, oa);
+        tc::wait_ld();
+        tc::st8(taddr, oa);            // hi of points 0..15   -> columns 0..7
+        tc::st8(taddr + 16, oa + 8);   // lo of points 0..15   -> columns 16..23 (S already loaded)
+        const bool more = t + 1 < t1;
+        const uint32_t rn = r + 1 == NB ? 0 : r + 1;
+        const uint32_t phn = r + 1 == NB ? ph ^ 1 : ph;
+        if (more) {
+          ce = prof_clock();
+          epi_wait(sfull0 + 8 * rn, phn);
+          es += prof_clock() - ce;
+          tc::fence_after();
+          tc::ld16(tmem + lane_off + rn * NT + w * 32, va);
+        }
+        convert16(vb, 16, dc, diag, ob);
+        tc::st8(taddr + 8, ob);        // hi of points 16..31  -> columns 8..15
+        tc::st8(taddr + 24, ob + 8);   // lo of points 16..31  -> columns 24..31
+        ce = prof_clock();
+        tc::wait_st();
+        tc::wait_ld();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(pfull_leader + 8 * r);
+        r = rn;
+        ph = phn;
+        const unsigned long long ca = prof_clock();
+        ea += ca - ce;
+        if (pend) drain();
+        ed += prof_clock() - ca;
+        if (seg_j == kSeg - 1 || t + 1 == t1) {
+          pend = true;
+          pend_last = t + 1 == t1;
+          pend_live = live;
+          pend_dst = dst;
+          seg_j = 0;
+        } else {
+          ++seg_j;
+        }
+      }
+#else
+      for (int64_t t = t0; t < t1; ++t) {
+        ce = prof_clock();
+        epi_wait(sfull0 + 8 * r, ph);
+        tc::fence_after();
+        const unsigned long long cs = prof_clock();
         es += cs - ce;
         const uint32_t taddr = tmem + lane_off + r * NT + w * 32;
         uint32_t v[32];
@@ -384,14 +513,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::wait_st();
         tc::fence_before();
         __syncwarp();
-        const unsigned long long cw2 = clock64();
+        const unsigned long long cw2 = prof_clock();
         ec += cw2 - cs;
         if (lane == 0) tc::mbar_arrive_cluster(pfull_leader + 8 * r);
         if (++r == NB) { r = 0; ph ^= 1; }
-        const unsigned long long ca = clock64();
+        const unsigned long long ca = prof_clock();
         ea += ca - cw2;
         if (pend) drain();
-        ed += clock64() - ca;
+        ed += prof_clock() - ca;
         if (seg_j == kSeg - 1 || t + 1 == t1) {
           pend = true;
           pend_last = t + 1 == t1;
@@ -402,6 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ++seg_j;
         }
       }
+#endif
     }
     if (pend) drain();
     if (p.prof && warp == 4 && lane == 0) {
@@ -415,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::cluster_sync();  // the peer's TMEM/barriers stay live until both CTAs are done
   tc::fence_after();
-  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * 16 + 11] = clock64() - kstart;
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * 16 + 11] = prof_clock() - kstart;
   if (warp == 2) tc::tmem_dealloc_pair(tmem, 512);
 }
 

@@ -30,6 +30,8 @@ __global__ void probe(float *out, int iters, unsigned long long *cyc) {
       if constexpr (OP == 11) { asm volatile("tanh.approx.f32 %0, %0;" : "+f"(v[i])); }
       if constexpr (OP == 12) { asm volatile("sqrt.approx.ftz.f32 %0, %0;" : "+f"(v[i])); }
       if constexpr (OP == 13) { double dd = v[i]; asm volatile("fma.rn.f64 %0, %0, 0d3FF0000000000001, 0d3FE0000000000000;" : "+d"(dd)); v[i] = float(dd); }
+      if constexpr (OP == 16) { asm volatile("and.b32 %0, %0, 0xFFFFE001;" : "+r"(u[i])); }
+      if constexpr (OP == 17) { float e; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(v[i])); float h = __uint_as_float(__float_as_uint(e) & 0xFFFFE000u); float l = e - h; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(h), "f"(l)); v[i] = __uint_as_float(u[i]) + 1e-3f; }
       if constexpr (OP == 15) { asm volatile("fma.rn.f64 %0, %0, 0d3FF0000000000001, 0d3FE0000000000000;" : "+d"(dv[i])); }
       if constexpr (OP == 14) { double dd; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(dd) : "f"(v[i])); asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(v[i]) : "d"(dd)); }
     }
@@ -46,12 +48,12 @@ int main() {
   const int warps = 16, iters = 4096, blocks = 148;
   cudaMalloc(&out, blocks * warps * 32 * 4);
   cudaMalloc(&cyc, blocks * 8);
-  const char *names[] = {"ex2.ftz", "rsqrt", "cvt.f16x2.f32", "cvt.f32.f16", "fadd", "fmax", "ex2+fadd", "ex2+cvtpack", "ffma", "ex2(noftz)", "ex2.bf16x2", "tanh", "sqrt", "dfma(+2cvt)", "cvt f32<->f64", "dfma"};
-  for (int op = 13; op < 16; ++op) {
+  const char *names[] = {"ex2.ftz", "rsqrt", "cvt.f16x2.f32", "cvt.f32.f16", "fadd", "fmax", "ex2+fadd", "ex2+cvtpack", "ffma", "ex2(noftz)", "ex2.bf16x2", "tanh", "sqrt", "dfma(+2cvt)", "cvt f32<->f64", "dfma", "lop3", "rbf-entry-chain"};
+  for (int op = 0; op < 18; ++op) {
     for (int rep = 0; rep < 2; ++rep) {
       switch (op) {
 #define L(K) case K: probe<K><<<blocks, warps * 32>>>(out, iters, cyc); break;
-        L(0) L(1) L(2) L(3) L(4) L(5) L(6) L(7) L(8) L(9) L(10) L(11) L(12) L(13) L(14) L(15)
+        L(0) L(1) L(2) L(3) L(4) L(5) L(6) L(7) L(8) L(9) L(10) L(11) L(12) L(13) L(14) L(15) L(16) L(17)
       }
     }
     cudaDeviceSynchronize();
