@@ -374,14 +374,15 @@ def run_e2e(args, prob, spec, dev):
     t3 = time.perf_counter()
     state._e.close()
     b, r, m = CONFIG["b"], CONFIG["r"], CONFIG["m"]
-    # pinned host->device per step: block ids, sketch Omega, power start, W and
-    # Woodbury factors, coefficients, rho; device->host: 3 r x r Gram blocks + eta
-    per_iter_h2d = b * 8 + b * r * 8 + b * 8 + 2 * r * r * 8 + 2 * r * 8 + 8
+    # pinned host->device per step: block ids, the omega stream's PCG64 state (the
+    # sketch Omega is drawn on the GPU), power start, W and Woodbury factors,
+    # coefficients, rho; device->host: 3 r x r Gram blocks + eta
+    per_iter_h2d = b * 8 + 4 * 8 + b * 8 + 2 * r * r * 8 + 2 * r * 8 + 8
     per_iter_d2h = 3 * r * r * 8 + 8
     return {"value": K / (t2 - t1), "unit": "iters/s",
             "h2d_bytes_per_step": int(per_iter_h2d), "d2h_bytes_per_step": int(per_iter_d2h),
             "region": f"{K} x adasap_step through the public API after {Wu} warm-up steps "
-                      "(host RNG + pinned H2D of the step inputs + stepsize read to host each "
+                      "(host RNG seeding + block draw, pinned H2D of the step inputs, stepsize read to host each "
                       "step); setup (X, Y host->device) and the final W readback are timed "
                       "separately",
             "seconds": t2 - t1, "setup_s": t_setup, "w_readback_s": t3 - t2,

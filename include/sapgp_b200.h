@@ -24,6 +24,8 @@
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
+ *   sap_normal_fill     <- substream(seed, "omega", t).standard_normal  solvers.py:384,
+ *                          rng.py:14-24 (numpy PCG64 + ziggurat, bit-exact)
  *   sap_krows_tc (+ sap_tc_points, sap_tc_gather_rows, sap_tc_gather_cols, sap_z_operand)
  *                       <- the same col_dist_matmul product on the 5th-gen
  *                          tensor cores (the solver's Phase I, solvers.py:377)
@@ -193,6 +195,22 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
                  const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,
                  size_t ws_bytes, void *stream);
+
+/*
+ * Device-side numpy Generator.standard_normal (replaces the host draw of the
+ * Nystrom test matrix, substream(seed, "omega", t).standard_normal((b, r)),
+ * solvers.py:384 via rng.py:14-24). states: device array [nstreams][4] of
+ * u64 = PCG64 (state_hi, state_lo, inc_hi, inc_lo) as numpy's
+ * bit_generator.state reports them for a fresh generator. Writes the first
+ * `count` normals of stream s to out[s*ldo + i] (fp64), the same values
+ * numpy draws (csrc/rng.cu). count <= 2^20. After the stream is done,
+ * *sap_normal_status(ws) (a device int) is 0 (ok) or nonzero (raw words ran out /
+ * too many rejection draws: fall back to the host draw).
+ */
+size_t sap_normal_workspace(int64_t count, int nstreams);
+int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double *out, int64_t ldo,
+                    void *ws, size_t ws_bytes, void *stream);
+int *sap_normal_status(void *ws);
 
 #ifdef __cplusplus
 }

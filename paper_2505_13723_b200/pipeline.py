@@ -4,7 +4,7 @@ In one ADASAP iteration t (solvers.py:361-403) everything except the
 block-row product and the update depends only on (seed, t) and X:
 
     B_t      = sort(substream(seed, "block", t).choice(n, b))    solvers.py:375
-    Omega_t  = substream(seed, "omega", t).standard_normal((b, r)) :384
+    Omega_t  = substream(seed, "omega", t).standard_normal((b, r)) :384  (drawn on the GPU)
     sketch   = K[B,B] Omega_t                                     :385
     (U, S)   = rand_nystrom_retry(sketch, Omega_t, r)             :386
     rho      = S[-1] + lam                                         :387
@@ -38,7 +38,7 @@ import torch
 from . import kernels as K
 from .errors import NumericalError
 from .randnla import factor_gram_retry, woodbury_core
-from .rng import block_hash, substream, uniform_block
+from .rng import DeviceNormals, block_hash, pcg64_words, substream, uniform_block
 
 
 @dataclass
@@ -79,7 +79,12 @@ class _Slot:
         self.RAg = torch.empty((L, bpad, ka), dtype=f32, device=dev) if ka else None
         pin = torch.cuda.is_available()
         self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
-        self.h_omega = torch.empty((L, b, max(r, 1)), dtype=f64, pin_memory=pin)
+        # Omega_t is drawn on the GPU from the omega stream's PCG64 state
+        # (csrc/rng.cu, numpy-exact); the host only seeds the streams
+        self.h_states = torch.empty((L, 4), dtype=i64, pin_memory=pin)
+        self.states = torch.empty((L, 4), dtype=i64, device=dev)
+        self.omega = torch.empty((L, b, r), dtype=f64, device=dev) if r else None
+        self.normals = DeviceNormals(b * r, L, dev) if r else None
         self.h_v0 = torch.empty((L, b), dtype=f64, pin_memory=pin)
         self.h_small = torch.empty((L, 3, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
         self.h_w = torch.empty((L, 2, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
@@ -217,8 +222,11 @@ class Lookahead:
             RAg=None if s.RAg is None else s.RAg[i])
 
     def check_flags(self):
-        """Raise if any power iteration failed (checked once, at the end)."""
+        """Raise if any power iteration or device normal draw failed (checked once,
+        at the end)."""
         for s in self.slots:
+            if s.normals is not None and int(s.normals.status()) != 0:
+                raise NumericalError("device normal draw ran out of raw stream words")
             if int(s.bad.max()) != 0:
                 raise NumericalError("power iteration failed (collapsed or nonpositive Rayleigh "
                                      "estimate; H is not PSD)")
@@ -235,7 +243,7 @@ class Lookahead:
             blk = uniform_block(seed, t, n, b).astype(np.int64)
             slot.h_block[i].numpy()[:] = blk
             if r:
-                slot.h_omega[i].numpy()[:] = substream(seed, "omega", t).standard_normal((b, r))
+                slot.h_states[i].numpy()[:] = pcg64_words(substream(seed, "omega", t))
             rng = substream(seed, "power", t)
             v = rng.standard_normal(b)
             nv = np.linalg.norm(v)
@@ -257,7 +265,11 @@ class Lookahead:
                 side.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
             slot.v0[:count].copy_(slot.h_v0[:count], non_blocking=True)
-            om = slot.h_omega[:count].to(self.dev, non_blocking=True) if r else None
+            om = None
+            if r:
+                slot.states[:count].copy_(slot.h_states[:count], non_blocking=True)
+                om = slot.omega[:count]
+                slot.normals.fill(slot.states, om.view(count, b * r), nstreams=count)
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
             sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
@@ -291,12 +303,12 @@ class Lookahead:
             ev.synchronize()
             tm2 = time.perf_counter()
             hs = slot.h_small[:count].numpy()
-            hom = slot.h_omega
+            dom = slot.omega
 
             def factor(i):
                 W, S, UtU = factor_gram_retry(hs[i, 0], hs[i, 1], hs[i, 2], r,
                                               omega_rank=lambda: np.linalg.matrix_rank(
-                                                  hom[i].numpy()))
+                                                  dom[i].cpu().numpy()))
                 rho_i = float(S[-1]) + self.lam
                 slot.h_w[i, 0].numpy()[:] = W
                 slot.h_w[i, 1].numpy()[:] = woodbury_core(S, UtU, rho_i)

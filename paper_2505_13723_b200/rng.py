@@ -35,3 +35,50 @@ def block_hash(block):
     """crc32 of the index bytes, the trace's cross-implementation check
     (solvers.py:250-251)."""
     return zlib.crc32(np.ascontiguousarray(block).tobytes())
+
+
+def pcg64_words(gen):
+    """PCG64 state of a fresh Generator as the 4 u64 words sap_normal_fill takes
+    (state_hi, state_lo, inc_hi, inc_lo), as signed int64 for a torch tensor."""
+    st = gen.bit_generator.state
+    if st["bit_generator"] != "PCG64" or st.get("has_uint32", 0):
+        raise ValueError("device normals need a fresh PCG64 generator")
+    words = []
+    for v in (st["state"]["state"], st["state"]["inc"]):
+        for w in (v >> 64, v & 0xFFFFFFFFFFFFFFFF):
+            words.append(w - (1 << 64) if w >= 1 << 63 else w)
+    return words
+
+
+class DeviceNormals:
+    """Generator.standard_normal on the GPU, bit-exact with numpy (csrc/rng.cu).
+
+    ``fill(states, out)`` writes the first ``count`` normals of each of the
+    ``nstreams`` PCG64 streams (rows of the int64 (nstreams, 4) device tensor
+    ``states``, see :func:`pcg64_words`) to the rows of ``out``
+    ((nstreams, >= count) float64, row stride ``out.stride(0)``): the draw
+    ``substream(seed, "omega", t).standard_normal((b, r))`` is row-major, so a
+    (b, r) array is filled by count = b * r (solvers.py:384)."""
+
+    def __init__(self, count, nstreams, device):
+        import torch
+        from . import _native as nat
+        self.nat = nat
+        self.count, self.nstreams = int(count), int(nstreams)
+        lib = nat.load()
+        nbytes = lib.sap_normal_workspace(self.count, self.nstreams)
+        self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=device)
+        assert lib.sap_normal_status(nat.ptr(self.ws)) == self.ws.data_ptr()
+
+    def fill(self, states, out, nstreams=None):
+        ns = self.nstreams if nstreams is None else int(nstreams)
+        if not 0 < ns <= self.nstreams:
+            raise ValueError("more streams than the workspace was sized for")
+        nat = self.nat
+        nat.check(nat.load().sap_normal_fill(nat.ptr(states), ns, self.count, nat.ptr(out),
+                                             out.stride(0), nat.ptr(self.ws),
+                                             self.ws.numel() * 8, nat.stream_handle()))
+
+    def status(self):
+        """Device int32 status of the last fill (0 = ok); reading it syncs."""
+        return self.ws.view(dtype=__import__("torch").int32)[0]
