@@ -20,9 +20,12 @@
 //   1. raw:      R[p] = output after p+1 LCG steps (jump-ahead per chunk)
 //   2. classify: for every position p, the outcome IF a normal starts at p:
 //                value, emitted or rejected, and how many words it consumes
-//   3. resolve:  one CTA per stream walks the ~0.7% non-trivial positions in
-//                order (shared memory) to find which positions actually start
-//                a draw, then a block scan assigns output indices.
+//   3. resolve:  one CTA per stream compacts the ~1.5% non-trivial positions
+//                (in order), decides which of them start a draw (clusters of
+//                positions within reach of each other are walked in parallel)
+//                and scans the words each start consumes without a value
+//   4. emit:     every position computes its output index from the nearest
+//                non-trivial position before it (binary search) and writes
 // Floating-point steps use explicit _rn intrinsics in numpy's operation order
 // (no FMA contraction, as in numpy's x86-64 baseline build). Exactness: every
 // fast-path and wedge draw is bit-identical to numpy (the wedge's accept test
@@ -31,6 +34,7 @@
 // 3.654, ~2.6e-4 of draws) calls log1p, where numpy's libm (glibc, an
 // ifunc-selected variant) and CUDA can round differently: measured 8 values
 // of 12.8M draws differ, each by 1 ulp (tests/test_device_rng.py pins that).
+#include <climits>
 #include <cstdint>
 
 #include "common.cuh"
@@ -112,7 +116,16 @@ __global__ void raw_kernel(const uint64_t *states, int64_t L, uint64_t *R) {
   }
 }
 
-__global__ void classify_kernel(const uint64_t *Rall, int64_t L, double *valall, int *codeall) {
+__global__ void __launch_bounds__(256) classify_kernel(const uint64_t *Rall, int64_t L,
+                                                      double *valall, int *codeall) {
+  // the tables are indexed by a per-thread layer: gathered from shared memory
+  // (divergent __constant__ reads serialise)
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  ki[threadIdx.x] = zig::ki[threadIdx.x];
+  wi[threadIdx.x] = zig::wi[threadIdx.x];
+  fi[threadIdx.x] = zig::fi[threadIdx.x];
+  __syncthreads();
   const int s = blockIdx.y;
   const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= L) return;
@@ -122,11 +135,11 @@ __global__ void classify_kernel(const uint64_t *Rall, int64_t L, double *valall,
   r >>= 8;
   const bool neg = (r & 1) != 0;
   const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-  double x = __dmul_rn(double(rabs), zig::wi[idx]);
+  double x = __dmul_rn(double(rabs), wi[idx]);
   if (neg) x = -x;
   double val = x;
   int code;
-  if (rabs < zig::ki[idx]) {
+  if (rabs < ki[idx]) {
     code = (1 << 30) | 1;
   } else if (idx == 0) {
     code = 0;  // runs past the generated words unless accepted below
@@ -141,8 +154,8 @@ __global__ void classify_kernel(const uint64_t *Rall, int64_t L, double *valall,
     }
   } else if (p + 1 < L) {
     const double u = next_double(R[p + 1]);
-    const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(zig::fi[idx - 1], -zig::fi[idx]), u),
-                                 zig::fi[idx]);
+    const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(fi[idx - 1], -fi[idx]), u),
+                                 fi[idx]);
     const bool acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x));
     code = (acc ? (1 << 30) : 0) | 2;
   } else {
@@ -152,14 +165,15 @@ __global__ void classify_kernel(const uint64_t *Rall, int64_t L, double *valall,
   codeall[s * L + p] = code;
 }
 
-// exclusive block scan of one int per thread (1024 threads); returns the total
+// Block-wide exclusive scans of one value per thread (1024 threads).
+template <bool MAX>
 __device__ int block_scan(int v, int *warp_sums, int &excl) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    if (lane >= o) x = MAX ? max(x, y) : x + y;
   }
   if (lane == 31) warp_sums[wid] = x;
   __syncthreads();
@@ -168,107 +182,182 @@ __device__ int block_scan(int v, int *warp_sums, int &excl) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
+      if (lane >= o) w = MAX ? max(w, y) : w + y;
     }
     warp_sums[lane] = w;  // inclusive
   }
   __syncthreads();
-  const int base = wid ? warp_sums[wid - 1] : 0;
-  excl = base + x - v;
+  const int base = wid ? warp_sums[wid - 1] : (MAX ? INT_MIN : 0);
+  const int xe = __shfl_up_sync(0xffffffffu, x, 1);  // exclusive within the warp
+  excl = lane ? (MAX ? max(base, xe) : base + xe) : base;
   const int total = warp_sums[31];
   __syncthreads();
   return total;
 }
 
+constexpr int kFast = (1 << 30) | 1;  // code of a one-word emitting draw
+constexpr int kChunkPos = 2048;       // positions per compaction chunk
+
+// Per-stream special list (global): pos, flags (bit0 start, bit1 emits), D
+// exclusive/inclusive (non-emitting positions before/through the entry's
+// range, counted over starts only), cover (prefix max of start range ends).
+struct Special {
+  int *pos, *flags, *dex, *din, *cover, *n;
+};
+__device__ __forceinline__ Special special_list(int *base, int s) {
+  int *b = base + size_t(s) * (5 * kMaxSpecial + 32);
+  return Special{b, b + kMaxSpecial, b + 2 * kMaxSpecial, b + 3 * kMaxSpecial,
+                 b + 4 * kMaxSpecial, b + 5 * kMaxSpecial};
+}
+
+// One CTA per stream: compact the non-trivial positions (ballot, in order),
+// find which of them start a draw (parallel over clusters of mutually
+// reachable positions, which are almost always single entries), then scan the
+// words each start wastes so every position knows its output index.
 __global__ void __launch_bounds__(kResolveThreads, 1)
-    resolve_kernel(const double *valall, const int *codeall, int64_t L, int64_t count,
-                   double *out, int64_t ldo, int *status) {
+    resolve_kernel(const int *codeall, int64_t L, int64_t count, int *splist, int *status) {
   extern __shared__ int sm[];
-  int *sp_pos = sm;                     // [kMaxSpecial] positions of non-trivial draws
-  int *sp_code = sp_pos + kMaxSpecial;  // [kMaxSpecial] their codes, then start flags
-  int *sp_end = sp_code + kMaxSpecial;  // [kMaxSpecial] covered-through (prefix max)
+  int *sp_pos = sm;                     // [kMaxSpecial]
+  int *sp_code = sp_pos + kMaxSpecial;  // [kMaxSpecial]
+  int *chunk_off = sp_code + kMaxSpecial;  // [kResolveThreads]
   __shared__ int warp_sums[32];
   const int s = blockIdx.x;
-  const double *val = valall + s * L;
   const int *code = codeall + s * L;
-  const int64_t per = (L + kResolveThreads - 1) / kResolveThreads;
-  const int64_t p0 = min(L, per * threadIdx.x), p1 = min(L, p0 + per);
-
-  // 1. compact the non-trivial positions, in order
-  int mine = 0;
-  for (int64_t p = p0; p < p1; ++p) mine += code[p] != ((1 << 30) | 1);
-  int off;
-  const int nsp = block_scan(mine, warp_sums, off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nchunks = int((L + kChunkPos - 1) / kChunkPos);  // <= 1024 (count <= 2^20)
+  // 1. count per chunk (warp per chunk, coalesced), scan, compact in order
+  for (int c = wid; c < nchunks; c += 32) {
+    int cnt = 0;
+    for (int64_t p = int64_t(c) * kChunkPos + lane; p < min(L, int64_t(c + 1) * kChunkPos); p += 32)
+      cnt += code[p] != kFast;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) chunk_off[c] = cnt;
+  }
+  __syncthreads();
+  int my = threadIdx.x < nchunks ? chunk_off[threadIdx.x] : 0, off;
+  const int nsp = block_scan<false>(my, warp_sums, off);
   if (nsp > kMaxSpecial) {
     if (threadIdx.x == 0) atomicMax(status, 2);
     return;
   }
-  for (int64_t p = p0; p < p1; ++p) {
-    const int c = code[p];
-    if (c != ((1 << 30) | 1)) {
-      sp_pos[off] = int(p);
-      sp_code[off] = c;
-      ++off;
-    }
-  }
+  if (threadIdx.x < nchunks) chunk_off[threadIdx.x] = off;
   __syncthreads();
-  // 2. walk them in order: a non-trivial position starts a draw iff the walk
-  //    reaches it (every position in between consumes exactly one word)
-  //    (the walk stops once `count` values are out: draws after that may run
-  //    past the generated words without harm)
-  if (threadIdx.x == 0) {
-    int cur = 0, cov = 0;
-    int64_t emitted = 0;
-    int k = 0;
-    for (; k < nsp; ++k) {
-      const int pos = sp_pos[k], c = sp_code[k];
-      if (pos >= cur) {
-        emitted += pos - cur;  // the one-word draws in between
-        if (emitted >= count) break;
-        if ((c & 0x3fffffff) == 0) {  // a draw needs words past the generated ones
-          atomicMax(status, 1);
-          cur = int(L);
-        } else {
-          cur = pos + (c & 0x3fffffff);
-          emitted += (c >> 30) & 1;
-        }
-        sp_code[k] = c | int(0x80000000u);  // starts
-        cov = cur;
+  for (int c = wid; c < nchunks; c += 32) {
+    int o = chunk_off[c];
+    for (int64_t p0 = int64_t(c) * kChunkPos; p0 < min(L, int64_t(c + 1) * kChunkPos); p0 += 32) {
+      const int64_t p = p0 + lane;
+      const int cd = p < L ? code[p] : kFast;
+      const unsigned m = __ballot_sync(0xffffffffu, cd != kFast);
+      if (cd != kFast) {
+        const int k = o + __popc(m & ((1u << lane) - 1));
+        sp_pos[k] = int(p);
+        sp_code[k] = cd;
       }
-      sp_end[k] = cov;  // positions < cov after the last start at or before k are consumed
+      o += __popc(m);
     }
-    for (; k < nsp; ++k) sp_end[k] = cov;
   }
   __syncthreads();
-  // 3. emitted values in order: count, scan, write
-  auto starts = [&](int64_t p, int &k) -> int {  // 1 = starts and emits
-    while (k < nsp && sp_pos[k] < p) ++k;
-    if (k < nsp && sp_pos[k] == p) {
-      const int c = sp_code[k];
-      return (c < 0 && (c & (1 << 30))) ? 1 : 0;
-    }
-    return (k == 0 || sp_end[k - 1] <= p) ? 1 : 0;  // trivial: emits unless consumed
+  // 2. starts: entry k is certainly a start when no earlier entry's range
+  //    reaches it (exclusive prefix max of pos + len); the thread owning such
+  //    a head walks its cluster up to the next head
+  const int per = (nsp + kResolveThreads - 1) / kResolveThreads;
+  const int k0 = min(nsp, per * int(threadIdx.x)), k1 = min(nsp, k0 + per);
+  auto reach = [&](int k) {
+    const int len = sp_code[k] & 0x3fffffff;
+    return len ? sp_pos[k] + len : int(L);  // len 0: the draw runs past the words
   };
-  int k0 = 0;
-  {  // first special at or after p0 (binary search)
-    int lo = 0, hi = nsp;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sp_pos[mid] < p0) lo = mid + 1; else hi = mid;
+  int rmax = INT_MIN;
+  for (int k = k0; k < k1; ++k) rmax = max(rmax, reach(k));
+  int rex;
+  block_scan<true>(rmax, warp_sums, rex);
+  // Heads in [k0, k1) (prefix max before k <= pos_k) are starts; the owning
+  // thread walks the cluster: cur = end of the last start's range, an entry at
+  // or past cur starts a draw, the next head (running prefix max <= its
+  // position) ends the cluster. Each entry's start bit (sp_code bit 31) has
+  // exactly one writer; reach() reads only the length bits.
+  {
+    int pm = rex;
+    for (int k = k0; k < k1; ++k) {
+      if (pm <= sp_pos[k]) {
+        sp_code[k] |= int(0x80000000u);
+        int cur = reach(k), pmw = max(pm, cur);
+        for (int j = k + 1; j < nsp; ++j) {
+          const int pj = sp_pos[j];
+          if (pmw <= pj) break;  // head of the next cluster
+          const int rj = reach(j);
+          if (pj >= cur) {
+            sp_code[j] |= int(0x80000000u);
+            cur = rj;
+          }
+          pmw = max(pmw, rj);
+        }
+      }
+      pm = max(pm, reach(k));
     }
-    k0 = lo;
   }
-  int k = k0, emit = 0;
-  for (int64_t p = p0; p < p1; ++p) emit += starts(p, k);
-  const int total = block_scan(emit, warp_sums, off);
-  if (total < count) {
-    if (threadIdx.x == 0) atomicMax(status, 1);
-    return;
+  __syncthreads();
+  // 3. non-emitting positions per start: the range's interior + the start
+  //    itself when rejected; exclusive sum -> D, prefix max of start ends -> cover
+  Special sp = special_list(splist, s);
+  int dsum = 0, cmax = 0;
+  for (int k = k0; k < k1; ++k) {
+    const int c = sp_code[k];
+    if (c < 0) {
+      const int r = reach(k);
+      dsum += (r - sp_pos[k] - 1) + ((c >> 30) & 1 ? 0 : 1);
+      cmax = max(cmax, r);
+    }
   }
-  k = k0;
-  double *o = out + s * ldo;
-  for (int64_t p = p0; p < p1 && off < count; ++p)
-    if (starts(p, k)) o[off++] = val[p];
+  int dex;
+  const int dtot = block_scan<false>(dsum, warp_sums, dex);
+  int cex;
+  block_scan<true>(cmax, warp_sums, cex);
+  cex = max(cex, 0);
+  for (int k = k0; k < k1; ++k) {
+    const int c = sp_code[k];
+    const bool st = c < 0;
+    const int r = reach(k);
+    const int nonemit = st ? (r - sp_pos[k] - 1) + ((c >> 30) & 1 ? 0 : 1) : 0;
+    sp.pos[k] = sp_pos[k];
+    sp.flags[k] = (st ? 1 : 0) | (st && ((c >> 30) & 1) ? 2 : 0);
+    sp.dex[k] = dex;
+    sp.din[k] = dex + nonemit;
+    if (st) cex = max(cex, r);
+    sp.cover[k] = cex;
+    // a start whose draw runs past the generated words matters only if its
+    // value would be one of the first `count`
+    if (st && (c & 0x3fffffff) == 0 && sp_pos[k] - dex < count) atomicMax(status, 1);
+    dex += nonemit;
+  }
+  if (threadIdx.x == 0) {
+    *sp.n = nsp;
+    if (L - dtot < count) atomicMax(status, 1);
+  }
+}
+
+// Every position writes its value at its output index (or nothing).
+__global__ void emit_kernel(const double *valall, int64_t L, int64_t count, const int *splist,
+                            double *out, int64_t ldo) {
+  const int s = blockIdx.y;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= L) return;
+  const Special sp = special_list(const_cast<int *>(splist), s);
+  const int nsp = *sp.n;
+  int lo = 0, hi = nsp;  // first entry with pos > p
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sp.pos[mid] <= p) lo = mid + 1; else hi = mid;
+  }
+  const int k = lo - 1;  // last entry with pos <= p
+  int64_t idx;
+  if (k >= 0 && sp.pos[k] == p) {
+    if (sp.flags[k] != 3) return;
+    idx = p - sp.dex[k];
+  } else {
+    if (k >= 0 && sp.cover[k] > p) return;
+    idx = p - (k >= 0 ? sp.din[k] : 0);
+  }
+  if (idx < count) out[s * ldo + idx] = valall[s * L + p];
 }
 
 }  // namespace rng
@@ -280,7 +369,8 @@ extern "C" {
 
 size_t sap_normal_workspace(int64_t count, int nstreams) {
   const int64_t L = rng::raw_len(count);
-  return size_t(nstreams) * size_t(L) * (8 + 8 + 4) + 256;
+  return 256 + size_t(nstreams) * size_t(L) * (8 + 8 + 4) +
+         size_t(nstreams) * (5 * rng::kMaxSpecial + 32) * sizeof(int);
 }
 
 int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double *out, int64_t ldo,
@@ -297,6 +387,7 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
   uint64_t *R = reinterpret_cast<uint64_t *>(w + 256);
   double *val = reinterpret_cast<double *>(w + 256 + size_t(nstreams) * L * 8);
   int *code = reinterpret_cast<int *>(w + 256 + size_t(nstreams) * L * 16);
+  int *splist = reinterpret_cast<int *>(w + 256 + size_t(nstreams) * L * 20);
   int rc;
   if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
     return fail(SAP_ERR_DEVICE, "normal_fill: memset failed");
@@ -306,16 +397,16 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
     rng::raw_kernel<<<grid, 256, 0, st>>>(states, L, R);
     if ((rc = check_launch("normal_raw_kernel")) != SAP_OK) return rc;
   }
-  {
-    dim3 grid(unsigned((L + 255) / 256), unsigned(nstreams));
-    rng::classify_kernel<<<grid, 256, 0, st>>>(R, L, val, code);
-    if ((rc = check_launch("normal_classify_kernel")) != SAP_OK) return rc;
-  }
-  const int smem = 3 * rng::kMaxSpecial * int(sizeof(int));
+  const dim3 pgrid(unsigned((L + 255) / 256), unsigned(nstreams));
+  rng::classify_kernel<<<pgrid, 256, 0, st>>>(R, L, val, code);
+  if ((rc = check_launch("normal_classify_kernel")) != SAP_OK) return rc;
+  const int smem = (2 * rng::kMaxSpecial + rng::kResolveThreads) * int(sizeof(int));
   cudaFuncSetAttribute(rng::resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  rng::resolve_kernel<<<nstreams, rng::kResolveThreads, smem, st>>>(val, code, L, count, out, ldo,
+  rng::resolve_kernel<<<nstreams, rng::kResolveThreads, smem, st>>>(code, L, count, splist,
                                                                    status);
-  return check_launch("normal_resolve_kernel");
+  if ((rc = check_launch("normal_resolve_kernel")) != SAP_OK) return rc;
+  rng::emit_kernel<<<pgrid, 256, 0, st>>>(val, L, count, splist, out, ldo);
+  return check_launch("normal_emit_kernel");
 }
 
 // status word of the last sap_normal_fill on this workspace (device pointer,

@@ -8,7 +8,7 @@ import paper_2505_13723_b200 as sap
 from paper_2505_13723_b200 import synthetic
 from paper_2505_13723_b200.solvers import AdasapEngine
 n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
-prob = synthetic.make_problem(n, d, "matern32", m, seed=0, lam=1e-2, device="cuda", rhs="noise")
+prob = synthetic.make_problem(n, d, os.environ.get("FAM", "matern32"), m, seed=0, lam=1e-2, device="cuda", rhs="noise")
 o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
 cfg = sap.RunConfig(lam=prob.lam, blocksize=b, nystrom_rank=r, residual_every=0, max_iters=80)
 eng = AdasapEngine(o, prob.Y, cfg, sap.resolve_accel(cfg, n, b), total=80)
