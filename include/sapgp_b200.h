@@ -24,6 +24,7 @@
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
+ *   sap_sdd_update      <- sdd_solve's momentum/averaging step  solvers.py:487-493
  *   sap_normal_fill     <- substream(seed, "omega", t).standard_normal  solvers.py:384,
  *                          rng.py:14-24 (numpy PCG64 + ziggurat, bit-exact)
  *   sap_krows_tc (+ sap_tc_points, sap_tc_gather_rows, sap_tc_gather_cols, sap_z_operand)
@@ -195,6 +196,18 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
                  const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,
                  size_t ws_bytes, void *stream);
+
+/*
+ * SDD step (solvers.py:463-516, the stochastic-dual-descent baseline on the
+ * same block product): with V, W, E column-major (ldv >= rows),
+ *   V[j] = momentum*V[j] - eta*g[i] for owned block rows j = loc[i] >= 0,
+ *   V[j] = momentum*V[j] elsewhere;  W += V;  E += avg*(W - E).
+ * VB (b x m fp32) and pos (rows ints, all -1 on entry and on return) are
+ * caller workspace.
+ */
+int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int m,
+                   const int64_t *loc, int64_t b, const double *g, int64_t ldg, double eta,
+                   double momentum, double avg, float *VB, int *pos, void *stream);
 
 /*
  * Device-side numpy Generator.standard_normal (replaces the host draw of the

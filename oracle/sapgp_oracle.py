@@ -405,6 +405,89 @@ def rmse(pred, truth):
     return float(np.sqrt(np.mean((pred - truth) ** 2)))
 
 
+# ---------------------------------------------------------------------------
+# baselines on the same operator  (solvers.py:463-584)
+
+SDD_MOMENTUM = 0.9  # solvers.py:25
+
+
+def _due(every, t, total):
+    """solvers.py:351-354."""
+    if every <= 0:
+        return t == total - 1
+    return (t + 1) % every == 0 or t == total - 1
+
+
+def sdd_solve(pts, lam, Y, iters, seed, b, scale=10.0, residual_every=0, workers=1):
+    """solvers.py:463-516 -- block stochastic dual descent: raw block gradient,
+    stepsize scale/n, heavy-ball momentum 0.9, geometric averaging 100/T.
+    Returns (estimate, residual trace (nan where not due), crc32 per block)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    Y2 = Y[:, None] if Y.ndim == 1 else Y
+    n = pts.n
+    eta = scale / n
+    avg = min(1.0, 100.0 / iters)
+    w = np.zeros_like(Y2)
+    vel = np.zeros_like(Y2)
+    est = np.zeros_like(Y2)
+    res, crcs = [], []
+    for t in range(iters):
+        block = uniform_block(seed, t, n, b)
+        grad = col_dist_matmul(pts, w, block, workers) + lam * w[block] - Y2[block]
+        vel *= SDD_MOMENTUM
+        vel[block] -= eta * grad
+        w += vel
+        est += avg * (w - est)
+        res.append(relative_residual(pts, lam, est, Y2) if _due(residual_every, t, iters)
+                   else math.nan)
+        crcs.append(block_crc(block))
+    return (est[:, 0] if Y.ndim == 1 else est), np.array(res), np.array(crcs, dtype=np.int64)
+
+
+def pcg_solve(pts, lam, Y, iters, seed, rank, tol=1e-6):
+    """solvers.py:519-584 -- CG on (K + lam I) W = Y with a global rank-r
+    Nystrom preconditioner (Omega from substream(seed, "omega"), sketch K Omega),
+    per-column recurrences, columns frozen once below tol. Returns (X,
+    residual trace, iterations)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    Y2 = Y[:, None] if Y.ndim == 1 else Y
+    n = pts.n
+    if rank > 0:
+        omega = substream(seed, "omega").standard_normal((n, rank))
+        U, S = rand_nystrom_retry(full_matmul(pts, omega), omega, rank)
+        rho = float(S[-1]) + lam
+    else:
+        U, S, rho = np.zeros((n, 0)), np.zeros(0), 1.0
+    tiny = np.finfo(np.float64).tiny
+    X = np.zeros_like(Y2)
+    R = Y2.copy()
+    Zp = apply_inv(U, S, rho, R)
+    P = Zp.copy()
+    rz = np.einsum("ij,ij->j", R, Zp)
+    cn = np.maximum(np.linalg.norm(Y2, axis=0), tiny)
+    yn = max(np.linalg.norm(Y2), tiny)
+    res, done = [], 0
+    for t in range(iters):
+        active = np.linalg.norm(R, axis=0) / cn > tol
+        if not np.any(active):
+            break
+        AP = full_matmul(pts, P) + lam * P
+        pap = np.einsum("ij,ij->j", P, AP)
+        if np.any(pap[active] <= 0.0):
+            raise OracleError("numerical", "conjugate gradient breakdown")
+        alpha = np.where(active, rz / np.where(pap > 0.0, pap, 1.0), 0.0)
+        X += alpha * P
+        R -= alpha * AP
+        Zp = apply_inv(U, S, rho, R)
+        rz_new = np.einsum("ij,ij->j", R, Zp)
+        beta = np.where(active, rz_new / np.where(rz > 0.0, rz, 1.0), 0.0)
+        P = Zp + beta * P
+        rz = rz_new
+        done = t + 1
+        res.append(float(np.linalg.norm(R) / yn))
+    return (X[:, 0] if Y.ndim == 1 else X), np.array(res), done
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))

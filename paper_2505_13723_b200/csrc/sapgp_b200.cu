@@ -138,6 +138,42 @@ __global__ void pq_update_kernel(float *P, float *Q, int64_t ldp, const int64_t 
   }
 }
 
+// ---------------------------------------------------------------------------
+// SDD (solvers.py:463-516): velocity *= 0.9; velocity[B] -= eta*grad;
+// w += velocity; estimate += avg * (w - estimate), as a block scatter of the
+// block rows' new velocity plus ONE dense pass over (V, W, E).
+
+__global__ void sdd_block_kernel(const float *V, int64_t ldv, const int64_t *loc, int64_t b, int m,
+                                 const double *g, int64_t ldg, double eta, double momentum,
+                                 float *VB, int *pos) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b * m) return;
+  const int64_t i = e / m;
+  const int c = int(e % m);
+  const int64_t j = loc[i];
+  if (j < 0) return;
+  // fp32 like the dense pass, in the reference's order: (0.9 v) - eta g
+  const float vm = float(momentum) * V[int64_t(c) * ldv + j];
+  VB[i * m + c] = vm - float(eta * g[i * ldg + c]);
+  if (c == 0) pos[j] = int(i);
+}
+
+__global__ void sdd_dense_kernel(float *V, float *W, float *E, int64_t ldv, int64_t rows, int m,
+                                 const float *VB, int *pos, float momentum, float avg) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= rows) return;
+  const int p = pos[j];
+  for (int c = 0; c < m; ++c) {
+    const int64_t o = int64_t(c) * ldv + j;
+    const float v = p >= 0 ? VB[int64_t(p) * m + c] : momentum * V[o];
+    const float w = W[o] + v;
+    V[o] = v;
+    W[o] = w;
+    E[o] += avg * (w - E[o]);
+  }
+  if (p >= 0) pos[j] = -1;  // clean for the next iteration
+}
+
 __global__ void combine_kernel(float *out, int64_t ldo, const float *P, const float *Q,
                                int64_t ldp, int64_t n, int m, float a, float bq) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -395,6 +431,24 @@ int sap_combine(float *out, int64_t ldo, const float *P, const float *Q, int64_t
   combine_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(out, ldo, P, Q, ldp, n, m,
                                                                     float(a), float(b));
   return check_launch("combine_kernel");
+}
+
+int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int m,
+                   const int64_t *loc, int64_t b, const double *g, int64_t ldg, double eta,
+                   double momentum, double avg, float *VB, int *pos, void *stream) {
+  if (rows < 0 || m <= 0 || b < 0 || ldv < rows)
+    return fail(SAP_ERR_CONTRACT, "sdd_update: bad shape");
+  int rc;
+  if (b > 0) {
+    const int64_t tot = b * m;
+    sdd_block_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
+        V, ldv, loc, b, m, g, ldg, eta, momentum, VB, pos);
+    if ((rc = check_launch("sdd_block_kernel")) != SAP_OK) return rc;
+  }
+  if (rows == 0) return SAP_OK;
+  sdd_dense_kernel<<<unsigned((rows + 255) / 256), 256, 0, S(stream)>>>(
+      V, W, E, ldv, rows, m, VB, pos, float(momentum), float(avg));
+  return check_launch("sdd_dense_kernel");
 }
 
 }  // extern "C"

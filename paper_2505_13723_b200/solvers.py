@@ -575,12 +575,19 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
 def solve(oracle, Y, config, dpp_model=None, pool=None, on_iterate=None):
     """Dispatch on ``config.solver_id`` (solvers.py:591-615).
 
-    The B200 build implements the ADASAP hot path (``adasap``, ``adasap_i``);
-    the exact-SAP / SDD / PCG baselines are outside this build's scope."""
+    The B200 build implements the ADASAP hot path (``adasap``, ``adasap_i``)
+    and the SDD and Nystrom-PCG baselines on the same kernel (baselines.py);
+    exact SAP (a dense b x b Cholesky per iteration) is outside its scope."""
     if config.solver_id == "adasap":
         return adasap_solve(oracle, Y, config, on_iterate=on_iterate)
     if config.solver_id == "adasap_i":
         return adasap_solve(oracle, Y, config, identity_precond=True, on_iterate=on_iterate)
-    if config.solver_id in ("sap", "sdd", "pcg"):
+    if config.solver_id == "sdd":
+        from .baselines import sdd_solve
+        return sdd_solve(oracle, Y, config, pool=pool, on_iterate=on_iterate)
+    if config.solver_id == "pcg":
+        from .baselines import pcg_solve
+        return pcg_solve(oracle, Y, config, pool=pool, on_iterate=on_iterate)
+    if config.solver_id == "sap":
         raise ConfigError(f"solver {config.solver_id!r} is outside the B200 hot-path build")
     raise ConfigError(f"unknown solver {config.solver_id!r}")

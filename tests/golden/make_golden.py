@@ -18,6 +18,9 @@ Fixtures (all float64, reference arithmetic):
                      inputs are regenerated from seeds by the tests
   randnla.npz        Nystrom factor, Woodbury applies, power stepsize
   rng.npz            block crc32s / first draws for several (seed, t, n, b)
+  baselines.npz      the SDD and Nystrom-PCG baselines (solvers.py:463-584) on
+                     the config 1 problem: final estimates, residual traces,
+                     block crc32s
 """
 
 import os
@@ -140,6 +143,30 @@ def randnla():
         eta=np.array(eta))
 
 
+def baselines():
+    """sdd_solve and pcg_solve of the reference on the config 1 problem."""
+    n, d, b, m, lam, seed = 2000, 8, 200, 9, 1e-2, 0
+    prob = synthetic.make_problem(n, d, "rbf", m, seed=seed, lam=lam)
+    spec = sapgp.KernelSpec("rbf", prob.lengthscales, prob.variance)
+    orc = sapgp.KernelOracle(spec, prob.X, lam)
+    out = {}
+    cfg = sapgp.RunConfig(lam=lam, blocksize=b, solver_id="sdd", max_iters=400,
+                          residual_every=50, seed=seed, stepsize_scale=10.0)
+    res = rsol.solve(orc, prob.Y, cfg)
+    out["sdd_W"] = res.W
+    out["sdd_res"] = np.array([r.residual for r in res.trace.records])
+    out["sdd_crc"] = np.array([r.block_hash for r in res.trace.records], dtype=np.int64)
+    out["sdd_eta"] = np.array([r.stepsize for r in res.trace.records])
+    for tag, rank in (("pcg", 100), ("cg", 0)):
+        cfg = sapgp.RunConfig(lam=lam, solver_id="pcg", nystrom_rank=rank, max_iters=40,
+                              seed=seed, tol=1e-6)
+        res = rsol.solve(orc, prob.Y, cfg)
+        out[f"{tag}_W"] = res.W
+        out[f"{tag}_res"] = np.array([r.residual for r in res.trace.records])
+        out[f"{tag}_iters"] = np.array(res.iterations)
+    np.savez_compressed(os.path.join(HERE, "baselines.npz"), **out)
+
+
 def rng_fixture():
     rows = []
     for seed, n, b in ((0, 2000, 200), (0, 100_000, 1000), (0, 1_000_000, 2000),
@@ -156,6 +183,7 @@ def rng_fixture():
 if __name__ == "__main__":
     kernels_small()
     config1()
+    baselines()
     config2()
     randnla()
     rng_fixture()

@@ -104,3 +104,22 @@ def test_config1_full_solve():
     np.testing.assert_array_equal(crcs, g["crc"])
     np.testing.assert_allclose(etas, g["eta"], rtol=1e-7)
     np.testing.assert_allclose(W, g["final_W"], rtol=0, atol=1e-6 * np.abs(g["final_W"]).max())
+
+
+def test_oracle_baselines_match_reference():
+    """SDD and (P)CG restatements against the reference's own runs
+    (tests/golden/baselines.npz, solvers.py:463-584)."""
+    g = np.load(os.path.join(GOLDEN, "baselines.npz"))
+    c1 = np.load(os.path.join(GOLDEN, "config1.npz"))
+    pts = orc.Points("rbf", c1["ls"], 1.0, c1["X"])
+    est, res, crcs = orc.sdd_solve(pts, 1e-2, c1["Y"], 400, 0, 200, 10.0, residual_every=50,
+                                   workers=4)
+    assert np.array_equal(crcs, g["sdd_crc"])
+    np.testing.assert_allclose(est, g["sdd_W"], rtol=0, atol=1e-9 * np.abs(g["sdd_W"]).max())
+    np.testing.assert_allclose(res, g["sdd_res"], rtol=1e-9)
+    for tag, rank in (("pcg", 100), ("cg", 0)):
+        X, res, it = orc.pcg_solve(pts, 1e-2, c1["Y"], 40, 0, rank)
+        assert it == int(g[f"{tag}_iters"])
+        np.testing.assert_allclose(X, g[f"{tag}_W"], rtol=0,
+                                   atol=1e-7 * np.abs(g[f"{tag}_W"]).max())
+        np.testing.assert_allclose(res, g[f"{tag}_res"], rtol=1e-6)
