@@ -203,7 +203,7 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
  *   V[j] = momentum*V[j] - eta*g[i] for owned block rows j = loc[i] >= 0,
  *   V[j] = momentum*V[j] elsewhere;  W += V;  E += avg*(W - E).
  * VB (b x m fp32) and pos (rows ints, all -1 on entry and on return) are
- * caller workspace.
+ * caller workspace; rows and ldv are multiples of 4 (pad rows are zero).
  */
 int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int m,
                    const int64_t *loc, int64_t b, const double *g, int64_t ldg, double eta,

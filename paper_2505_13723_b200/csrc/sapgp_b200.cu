@@ -158,20 +158,33 @@ __global__ void sdd_block_kernel(const float *V, int64_t ldv, const int64_t *loc
   if (c == 0) pos[j] = int(i);
 }
 
-__global__ void sdd_dense_kernel(float *V, float *W, float *E, int64_t ldv, int64_t rows, int m,
-                                 const float *VB, int *pos, float momentum, float avg) {
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= rows) return;
-  const int p = pos[j];
+// four consecutive rows per thread (16-byte accesses; ldv is a multiple of 4)
+__global__ void sdd_dense_kernel(float *__restrict__ V, float *__restrict__ W,
+                                 float *__restrict__ E, int64_t ldv, int64_t rows4, int m,
+                                 const float *__restrict__ VB, int *__restrict__ pos,
+                                 float momentum, float avg) {
+  const int64_t j4 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j4 >= rows4) return;
+  const int4 p = reinterpret_cast<const int4 *>(pos)[j4];
+  const bool any = p.x >= 0 || p.y >= 0 || p.z >= 0 || p.w >= 0;
+#pragma unroll 4
   for (int c = 0; c < m; ++c) {
-    const int64_t o = int64_t(c) * ldv + j;
-    const float v = p >= 0 ? VB[int64_t(p) * m + c] : momentum * V[o];
-    const float w = W[o] + v;
-    V[o] = v;
-    W[o] = w;
-    E[o] += avg * (w - E[o]);
+    const int64_t o = int64_t(c) * ldv / 4 + j4;
+    float4 v = reinterpret_cast<const float4 *>(V)[o];
+    float4 w = reinterpret_cast<const float4 *>(W)[o];
+    float4 e = reinterpret_cast<const float4 *>(E)[o];
+    v.x = p.x >= 0 ? VB[int64_t(p.x) * m + c] : momentum * v.x;
+    v.y = p.y >= 0 ? VB[int64_t(p.y) * m + c] : momentum * v.y;
+    v.z = p.z >= 0 ? VB[int64_t(p.z) * m + c] : momentum * v.z;
+    v.w = p.w >= 0 ? VB[int64_t(p.w) * m + c] : momentum * v.w;
+    w.x += v.x; w.y += v.y; w.z += v.z; w.w += v.w;
+    e.x += avg * (w.x - e.x); e.y += avg * (w.y - e.y);
+    e.z += avg * (w.z - e.z); e.w += avg * (w.w - e.w);
+    reinterpret_cast<float4 *>(V)[o] = v;
+    reinterpret_cast<float4 *>(W)[o] = w;
+    reinterpret_cast<float4 *>(E)[o] = e;
   }
-  if (p >= 0) pos[j] = -1;  // clean for the next iteration
+  if (any) reinterpret_cast<int4 *>(pos)[j4] = make_int4(-1, -1, -1, -1);  // clean for the next step
 }
 
 __global__ void combine_kernel(float *out, int64_t ldo, const float *P, const float *Q,
@@ -446,8 +459,11 @@ int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int 
     if ((rc = check_launch("sdd_block_kernel")) != SAP_OK) return rc;
   }
   if (rows == 0) return SAP_OK;
-  sdd_dense_kernel<<<unsigned((rows + 255) / 256), 256, 0, S(stream)>>>(
-      V, W, E, ldv, rows, m, VB, pos, float(momentum), float(avg));
+  if (rows % 4 || ldv % 4)
+    return fail(SAP_ERR_CONTRACT, "sdd_update: rows and ldv must be multiples of 4");
+  const int64_t rows4 = rows / 4;
+  sdd_dense_kernel<<<unsigned((rows4 + 255) / 256), 256, 0, S(stream)>>>(
+      V, W, E, ldv, rows4, m, VB, pos, float(momentum), float(avg));
   return check_launch("sdd_dense_kernel");
 }
 

@@ -401,9 +401,26 @@ class KernelOracle:
         if star.d != self.d:
             raise ContractError("point dimension does not match the training inputs")
         Rcm = to_colmajor(W, self.n, self.device)
-        out = torch.empty((star.n, Rcm.shape[0]), dtype=torch.float32, device=self.device)
+        t, m = star.n, Rcm.shape[0]
+        out = torch.empty((t, m), dtype=torch.float32, device=self.device)
+        if self.use_tc(m) and t >= 16:
+            # test points as the rows of the tensor-core kernel: their row-form
+            # features, zero padded to whole 256-row tiles; no row ids, so no
+            # diagonal rule (kernels.py:161-176)
+            tcp = self.tc_points()
+            Xs64 = torch.as_tensor(np.asarray(Xstar, dtype=np.float64) if not torch.is_tensor(
+                Xstar) else Xstar, dtype=torch.float64).to(self.device).contiguous()
+            RAs = torch.zeros(((t + 255) // 256 * 256, tcp.ka), dtype=torch.float32,
+                              device=self.device)
+            inv = torch.as_tensor(np.broadcast_to(1.0 / self.spec.lengthscales,
+                                                  (self.d,)).copy(), device=self.device)
+            nat.call("sap_tc_points", nat.ptr(Xs64), t, self.d, nat.ptr(inv), self.spec.code,
+                     tcp.ka, nat.ptr(RAs), None, nat.stream_handle())
+            zop = ZOperand(m, self.n, self.device).fill(Rcm)
+            krows_tc(self.spec, tcp, RAs, t, None, zop, out)
+            return _finish(out, like_np, vector)
         krows_times(self.spec, self.points, star.Xs, star.sqn, None, Rcm, out,
-                    ws=self._workspace(star.n, Rcm.shape[0], self.n))
+                    ws=self._workspace(t, m, self.n))
         return _finish(out, like_np, vector)
 
 

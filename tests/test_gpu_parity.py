@@ -214,3 +214,22 @@ def test_large_block_trajectory_tensor_core_sketch(fam):
     etas = np.array([rec.stepsize for rec in res.trace.records])
     assert np.abs(etas - eta_ref).max() / np.abs(eta_ref).max() < 1e-4
     assert rel(res.W, W_ref) < 1e-3
+
+
+@pytest.mark.parametrize("fam", FAMILIES)
+def test_cross_matmul_tensor_path_matches_oracle(fam):
+    """Test-time K(X*, X) W on the tensor-core kernel (external rows, no
+    diagonal rule; kernels.py:161-176) against the CPU oracle, with a test
+    point equal to a training point (its kernel value is the variance too)."""
+    rng = np.random.default_rng(7)
+    n, d, t, m = 5000, 9, 300, 65
+    X = rng.standard_normal((n, d))
+    Xs = rng.standard_normal((t, d))
+    Xs[5] = X[17]
+    ls = np.full(d, 3.0)
+    W = rng.standard_normal((n, m))
+    o = sap.KernelOracle(sap.KernelSpec(fam, ls, 1.3), X, 1e-2)
+    assert o.use_tc(m)
+    got = o.cross_matmul(Xs, W)
+    ref = orc.cross_matmul(orc.Points(fam, ls, 1.3, X), ls, Xs, W)
+    assert rel(got, ref) < 1e-4
