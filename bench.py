@@ -369,6 +369,7 @@ def run_e2e(args, prob, spec, dev):
     for _ in range(K):
         state, eta, block = sap.adasap_step(o, state, Y, cfg, accel)
         etas.append(eta)  # a host float: the per-step device->host read
+    torch.cuda.synchronize()  # every step's device work is inside the timed region
     t2 = time.perf_counter()
     W = state.W
     t3 = time.perf_counter()
@@ -382,9 +383,9 @@ def run_e2e(args, prob, spec, dev):
     return {"value": K / (t2 - t1), "unit": "iters/s",
             "h2d_bytes_per_step": int(per_iter_h2d), "d2h_bytes_per_step": int(per_iter_d2h),
             "region": f"{K} x adasap_step through the public API after {Wu} warm-up steps "
-                      "(host RNG seeding + block draw, pinned H2D of the step inputs, stepsize read to host each "
-                      "step); setup (X, Y host->device) and the final W readback are timed "
-                      "separately",
+                      "(host RNG seeding + block draw, pinned H2D of the step inputs, the step's "
+                      "stepsize read to the host each step) and a final device synchronize; "
+                      "setup (X, Y host->device) and the final W readback are timed separately",
             "seconds": t2 - t1, "setup_s": t_setup, "w_readback_s": t3 - t2,
             "solve_iters_per_s": K / (t_setup + (t2 - t1) + (t3 - t2)),
             "finite": bool(np.isfinite(W).all() and np.isfinite(etas).all())}

@@ -70,24 +70,47 @@ __global__ void gather_points_kernel(const float *Xs, const float *sqn, int ldx,
 // result is bitwise symmetric: (rn_i + rn_j) - 2 sum_k a_k c_k is symmetric
 // term by term in IEEE arithmetic.
 
+// 32 x 32 output tile per 256-thread block: the tile's row and column points
+// are staged in shared memory once (column stride ldx + 1: conflict-free),
+// each thread computes four rows of one column. Same arithmetic order as the
+// block product's distance (fmaf over k, then the norms): K(i, j) and K(j, i)
+// are bitwise equal, so the block is exactly symmetric (kernels.py:129-136).
 template <int FAM, typename T>
-__global__ void ktile_kernel(const float *Ra, const float *rasqn, const int64_t *row_ids,
-                             int64_t na, const float *Rc, const float *rcsqn,
-                             const int64_t *col_ids, int64_t nc, int ldx, int d, float variance,
-                             T *out, int64_t ldo) {
-  const int64_t i = int64_t(blockIdx.y) * blockDim.y + threadIdx.y;
-  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= na || j >= nc) return;
-  float v;
-  if (row_ids && col_ids && row_ids[i] == col_ids[j]) {
-    v = variance;
-  } else {
-    float dot = 0.0f;
-    for (int k = 0; k < d; ++k) dot = fmaf(Ra[i * ldx + k], Rc[j * ldx + k], dot);
-    const float sq = fmaf(-2.0f, dot, rasqn[i] + rcsqn[j]);
-    v = variance * kernel_value<FAM>(sq);
+__global__ void __launch_bounds__(256)
+    ktile_kernel(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,
+                 const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc, int ldx,
+                 int d, float variance, T *out, int64_t ldo) {
+  extern __shared__ float sh[];
+  float *sA = sh;                  // [32][ldx + 1]
+  float *sC = sh + 32 * (ldx + 1);  // [32][ldx + 1]
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int64_t i0 = int64_t(blockIdx.y) * 32, j0 = int64_t(blockIdx.x) * 32;
+  for (int e = tid; e < 32 * ldx; e += 256) {
+    const int r = e / ldx, k = e % ldx;
+    sA[r * (ldx + 1) + k] = i0 + r < na ? Ra[(i0 + r) * ldx + k] : 0.0f;
+    sC[r * (ldx + 1) + k] = j0 + r < nc ? Rc[(j0 + r) * ldx + k] : 0.0f;
   }
-  out[i * ldo + j] = T(v);
+  __syncthreads();
+  const int64_t j = j0 + tx;
+  if (j >= nc) return;
+  const float csq = rcsqn[j];
+  const int64_t cid = col_ids ? col_ids[j] : -1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int li = ty + 8 * q;
+    const int64_t i = i0 + li;
+    if (i >= na) break;
+    float v;
+    if (row_ids && col_ids && row_ids[i] == cid) {
+      v = variance;
+    } else {
+      float dot = 0.0f;
+      for (int k = 0; k < d; ++k) dot = fmaf(sA[li * (ldx + 1) + k], sC[tx * (ldx + 1) + k], dot);
+      const float sq = fmaf(-2.0f, dot, rasqn[i] + csq);
+      v = variance * kernel_value<FAM>(sq);
+    }
+    out[i * ldo + j] = T(v);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -112,29 +135,43 @@ __global__ void grad_gather_kernel(const float *G, int64_t ldg, const float *P, 
   g[i * ldgo + c] = v;
 }
 
-__global__ void pq_update_kernel(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b,
-                                 int m, const double *D, int64_t ldd, const double *eta_dev,
-                                 double zp, double zq, double e0, double e1, float *WB,
-                                 int64_t ldwb, float *Pb, float *Qb) {
+// Block-row update of the lazy Nesterov state, threads laid out column-major
+// over (row i, column c): a warp covers 32 block rows of ONE column, so the per-column magnitude bounds
+// take one warp-reduced atomic per warp instead of one per element.
+__global__ void pq_update_cm_kernel(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b,
+                                    int m, const double *D, int64_t ldd, const double *eta_dev,
+                                    double zp, double zq, double e0, double e1, float *WB,
+                                    int64_t ldwb, float *Pb, float *Qb) {
+  const int64_t bw = (b + 31) / 32 * 32;  // rows padded to whole warps
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= b * m) return;
-  const int64_t i = e / m;
-  const int c = int(e % m);
-  const int64_t j = loc[i];
-  if (j < 0) return;
-  const double eta = eta_dev[0];
-  const double dd = D[i * ldd + c];
-  const int64_t o = int64_t(c) * ldp + j;
-  const double p = P[o];
-  const double q = Q ? double(Q[o]) : 0.0;
-  if (WB) WB[i * ldwb + c] = float(zp * p + zq * q - eta * dd);
-  const float pn = float(p + e0 * eta * dd);
-  P[o] = pn;
-  if (Pb) atomicMax(reinterpret_cast<int *>(Pb + c), __float_as_int(fabsf(pn)));
-  if (Q) {
-    const float qn = float(q + e1 * eta * dd);
-    Q[o] = qn;
-    if (Qb) atomicMax(reinterpret_cast<int *>(Qb + c), __float_as_int(fabsf(qn)));
+  if (e >= bw * m) return;  // warp-uniform: bw * m is a multiple of 32
+  const int c = int(e / bw);
+  const int64_t i = e % bw;
+  const int64_t j = i < b ? loc[i] : -1;
+  float pa = 0.0f, qa = 0.0f;
+  if (j >= 0) {
+    const double eta = eta_dev[0];
+    const double dd = D[i * ldd + c];
+    const int64_t o = int64_t(c) * ldp + j;
+    const double p = P[o];
+    const double q = Q ? double(Q[o]) : 0.0;
+    if (WB) WB[i * ldwb + c] = float(zp * p + zq * q - eta * dd);
+    const float pn = float(p + e0 * eta * dd);
+    P[o] = pn;
+    pa = fabsf(pn);
+    if (Q) {
+      const float qn = float(q + e1 * eta * dd);
+      Q[o] = qn;
+      qa = fabsf(qn);
+    }
+  }
+  if (Pb) {
+    const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(pa));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<int *>(Pb + c), int(mx));
+  }
+  if (Qb && Q) {
+    const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(qa));
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(reinterpret_cast<int *>(Qb + c), int(mx));
   }
 }
 
@@ -275,21 +312,22 @@ static int ktile_launch(const float *Ra, const float *rasqn, const int64_t *row_
                         void *stream) {
   if (na <= 0 || nc <= 0 || ldo < nc || ldx < d || d < 1)
     return fail(SAP_ERR_CONTRACT, "ktile: bad shape");
-  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 7) / 8));
+  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 31) / 32));
   cudaStream_t st = S(stream);
   const float var = float(variance);
+  const size_t smem = size_t(2 * 32 * (ldx + 1)) * sizeof(float);
   switch (family) {
     case SAP_RBF:
-      ktile_kernel<SAP_RBF, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids,
-                                                     nc, ldx, d, var, out, ldo);
+      ktile_kernel<SAP_RBF, T><<<grid, blk, smem, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
+                                                        col_ids, nc, ldx, d, var, out, ldo);
       break;
     case SAP_MATERN32:
-      ktile_kernel<SAP_MATERN32, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
-                                                          col_ids, nc, ldx, d, var, out, ldo);
+      ktile_kernel<SAP_MATERN32, T><<<grid, blk, smem, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
+                                                             col_ids, nc, ldx, d, var, out, ldo);
       break;
     case SAP_MATERN52:
-      ktile_kernel<SAP_MATERN52, T><<<grid, blk, 0, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
-                                                          col_ids, nc, ldx, d, var, out, ldo);
+      ktile_kernel<SAP_MATERN52, T><<<grid, blk, smem, st>>>(Ra, rasqn, row_ids, na, Rc, rcsqn,
+                                                             col_ids, nc, ldx, d, var, out, ldo);
       break;
     default: return fail(SAP_ERR_CONTRACT, "ktile: unknown family %d", family);
   }
@@ -430,8 +468,8 @@ int sap_pq_update(float *P, float *Q, int64_t ldp, const int64_t *loc, int64_t b
                   double e0, double e1, float *WB, int64_t ldwb, float *Pb, float *Qb,
                   void *stream) {
   if (b <= 0 || m <= 0) return fail(SAP_ERR_CONTRACT, "pq_update: bad shape");
-  const int64_t tot = b * m;
-  pq_update_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
+  const int64_t tot = (b + 31) / 32 * 32 * m;
+  pq_update_cm_kernel<<<unsigned((tot + 255) / 256), 256, 0, S(stream)>>>(
       P, Q, ldp, loc, b, m, D, ldd, eta_dev, zp, zq, e0, e1, WB, ldwb, Pb, Qb);
   return check_launch("pq_update_kernel");
 }

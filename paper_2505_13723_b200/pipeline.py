@@ -56,6 +56,7 @@ class IterPlan:
     eta_dev: torch.Tensor      # (1,) fp64 view
     S: np.ndarray
     RAg: torch.Tensor | None = None  # (bpad, ka) gathered tensor-core row features
+    eta_host: object = None          # () -> float: eta_t read back once its batch is produced
 
 
 class _Slot:
@@ -90,6 +91,7 @@ class _Slot:
         self.h_w = torch.empty((L, 2, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
         self.h_coef = torch.empty((L, max(r, 1)), dtype=f64, pin_memory=pin)
         self.h_rho = torch.empty(L, dtype=f64, pin_memory=pin)
+        self.h_eta = torch.empty(L, dtype=f64, pin_memory=pin)
         self.free = None      # event on the main stream: last consumer enqueued
         self.h2d_done = None  # event on the side stream: pinned inputs consumed
 
@@ -104,6 +106,7 @@ class _Batch:
     rho: np.ndarray
     S: list
     ready: torch.cuda.Event = field(default=None)
+    eta_ready: torch.cuda.Event = field(default=None)
 
 
 class Lookahead:
@@ -214,12 +217,18 @@ class Lookahead:
                 self._submit(self.k + 2)
         i = t - cur.t0
         s = cur.slot
+        ev, h_eta = cur.eta_ready, s.h_eta
+
+        def eta_host():
+            ev.synchronize()
+            return float(h_eta[i])
+
         return IterPlan(
             t=t, block=cur.blocks[i], crc=cur.crcs[i], block_dev=s.block_dev[i],
             loc_dev=s.loc_dev[i], Xb=s.Xb[i], rsq=s.rsq[i],
             U=None if s.U is None else s.U[i], Mc=None if s.Mc is None else s.Mc[i],
             rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i],
-            RAg=None if s.RAg is None else s.RAg[i])
+            RAg=None if s.RAg is None else s.RAg[i], eta_host=eta_host)
 
     def check_flags(self):
         """Raise if any power iteration or device normal draw failed (checked once,
@@ -349,10 +358,16 @@ class Lookahead:
             ready = torch.cuda.Event()
             ready.record(self.main)
             slot.h2d_done = ready  # pinned host buffers reusable after this point
+            # the batch's stepsizes to the host as soon as they exist: a caller
+            # that wants eta_t (adasap_step) waits for its batch's power
+            # iteration, not for the block products queued after it
+            slot.h_eta[:count].copy_(slot.eta[:count], non_blocking=True)
+            eta_ready = torch.cuda.Event()
+            eta_ready.record(self.main)
         if self.timings is not None:
             self.timings.append(dict(count=count, rng=tm1 - tm0, gpu_wait=tm2 - tm1,
                                      factor=tm3 - tm2, total=time.perf_counter() - tm0))
-        return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready)
+        return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready, eta_ready)
 
 
 class _Cols:

@@ -500,7 +500,10 @@ def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=Fal
     (state, eta, block) like the reference (eta read back from the device)."""
     eng = state._e
     plan = eng.step()
-    return state, float(eng.etas[eng.t - 1]), plan.block
+    # eta_t is produced ahead by the lookahead; reading it back does not wait
+    # for this step's block product (call torch.cuda.synchronize() or read W
+    # to wait for the iterate itself)
+    return state, plan.eta_host(), plan.block
 
 
 def make_state(oracle, Y, config, accel=None, identity_precond=False, total=None):
