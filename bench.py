@@ -175,6 +175,10 @@ class ClockSampler:
 # B200 arm
 
 
+def b_pad_rows(b):
+    return (b + 255) // 256 * 256  # block rows the CTA-pair kernel computes
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -290,14 +294,22 @@ def run_b200(args):
     # peak taken as half the measured bf16 peak (no tf32 figure is measured).
     tensor_pipe = None
     if eng.use_tc:
-        ka, nz = eng.tcp.ka, eng.zop.nz
-        t_entry = 2 * ka / (0.5 * bf16_peak * 1e12) + 3 * 2 * nz / (bf16_peak * 1e12)
+        ka, nz, half = eng.tcp.ka, eng.zop.nz, eng.tcp.half
+        g1_rate = bf16_peak if half else 0.5 * bf16_peak  # f16 features, else tf32 (half rate)
+        t_entry = 2 * ka / (g1_rate * 1e12) + 3 * 2 * nz / (bf16_peak * 1e12)
         ideal_ms = b * n_local * t_entry * 1e3
-        tensor_pipe = {"hw_flop_per_entry": {"tf32": 2 * ka, "f16": 6 * nz},
+        g1 = "f16" if half else "tf32"
+        tensor_pipe = {"hw_flop_per_entry": {"gemm1_" + g1: 2 * ka, "gemm2_f16": 6 * nz},
                        "ideal_ms_at_peak": ideal_ms, "frac": ideal_ms / kmean,
-                       "note": "time the tensor pipe needs for GEMM1 (tf32, ka=%d) + GEMM2 (3 "
+                       "note": "time the tensor pipe needs for GEMM1 (%s, ka=%d) + GEMM2 (3 "
                                "fp16 passes, nz=%d) at the measured bf16 peak (tf32 = half) "
-                               "over the measured kernel time" % (ka, nz)}
+                               "over the measured kernel time" % (g1, ka, nz)}
+        # the epilogue's special-function bound: ex2 (RBF) or rsqrt + ex2 (Matern) per
+        # kernel entry on the MUFU pipe (16 lanes/clk/SM, scripts/micro/pipes.cu)
+        mufu_ops = 1 if args.family == "rbf" else 2
+        mufu_ms = b_pad_rows(b) * n_local * mufu_ops / (16 * 148 * 1.965e9) * 1e3
+        tensor_pipe["mufu_bound_ms"] = mufu_ms
+        tensor_pipe["mufu_frac"] = mufu_ms / kmean
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, prob, spec, dev)

@@ -51,6 +51,7 @@ extern "C" {
 
 enum { SAP_OK = 0, SAP_ERR_CONTRACT = 1, SAP_ERR_NUMERICAL = 2, SAP_ERR_DEVICE = 3 };
 enum { SAP_RBF = 0, SAP_MATERN32 = 1, SAP_MATERN52 = 2 };
+#define SAP_TC_KA_F16 48
 
 int sap_abi_version(void);
 const char *sap_last_error(void);
@@ -188,10 +189,13 @@ int sap_tc_supported(int d, int m);
  * Tensor-core block-row product (tcgen05 + TMEM + TMA, sm_100a):
  * out[i, c] (=, or +=) variance * sum_j k(row_i, col_j) Z[j, c] with rows
  * RAg ([bpad][ka], bpad a multiple of 128), columns CA ([ncols][ka]) and Z
+ * (features fp32 for ka = 32 or 64; ka = SAP_TC_KA_F16 means 32 fp16
+ * features per point -- the same tf32-rounded values, exact in fp16 -- and
+ * needs bpad a multiple of 256; the distance GEMM then runs kind::f16)
  * given by sap_z_operand. Diagonal rule as sap_krows_times (row_ids vs
  * col_base + j). nz <= 128.
  */
-int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64_t bpad,
+int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
                  const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
                  const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,

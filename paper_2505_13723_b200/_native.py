@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("SAP_LIB_PATH") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "_lib", "libsapgp_b200.so")
 
 SAP_OK, SAP_ERR_CONTRACT, SAP_ERR_NUMERICAL, SAP_ERR_DEVICE = 0, 1, 2, 3
+SAP_TC_KA_F16 = 48  # include/sapgp_b200.h: 32 fp16 features per point
 FAMILY_CODES = {"rbf": 0, "matern32": 1, "matern52": 2}
 ABI_VERSION = 1
 

@@ -141,7 +141,7 @@ class SddEngine:
         if self.use_tc:
             self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi)
             self.zop = ZOperand(m, nl, self.dev)
-            self.RAg = torch.empty(((b + 255) // 256 * 256, self.tcp.ka), dtype=f32,
+            self.RAg = torch.empty(((b + 255) // 256 * 256, self.tcp.ka), dtype=self.tcp.dtype,
                                    device=self.dev)
             need = nat.load().sap_krows_tc_workspace(b, m, nl)
         else:

@@ -250,7 +250,8 @@ EncodeFn encode_fn() {
 }
 
 bool make_map(CUtensorMap *m, CUtensorMapDataType dt, const void *base, uint64_t inner,
-              uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+              uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -258,7 +259,7 @@ bool make_map(CUtensorMap *m, CUtensorMapDataType dt, const void *base, uint64_t
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   return fn(m, dt, 2, const_cast<void *>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -387,17 +388,21 @@ size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols) {
   return size_t(s) * size_t(b) * size_t(m) * sizeof(float);
 }
 
-int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64_t bpad,
+int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
                  const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
                  const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,
                  size_t ws_bytes, void *stream) {
-  if (b <= 0 || m <= 0 || ncols <= 0 || (ka != 32 && ka != 64) || nz % 16 || nz < m ||
+  const bool half = ka == tck2::kKaF16;  // 32 fp16 features per point
+  if (b <= 0 || m <= 0 || ncols <= 0 || (ka != 32 && ka != 64 && !half) || nz % 16 || nz < m ||
       nz > 128 || bpad % BM || bpad < b || ldz % 8 || ldz < ncols || ncols > INT32_MAX)
     return fail(SAP_ERR_CONTRACT, "krows_tc: bad shape b=%lld m=%d nz=%d ncols=%lld ka=%d",
                 (long long)b, m, nz, (long long)ncols, ka);
   if (ldo < m) return fail(SAP_ERR_CONTRACT, "krows_tc: ldo < m");
   const bool pair = use_pair(nz, ka) && bpad % (2 * BM) == 0;
+  if (half && !pair)
+    return fail(SAP_ERR_CONTRACT, "krows_tc: fp16 features need the CTA-pair kernel "
+                "(bpad %% 256 == 0, nz=%d)", nz);
   const int nt = pair ? tck2::NT : NT;
   const int64_t tiles = (ncols + nt - 1) / nt;
   Params p{};
@@ -433,8 +438,16 @@ int sap_krows_tc(const float *CA, int64_t ncols, int ka, const float *RAg, int64
   const uint32_t xbox = pair ? tck2::NT / 2 : NT;
   const uint32_t zbox = pair ? nz / 2 : nz;
   CUtensorMap tm_rows, tm_cols, tm_zhi, tm_zlo;
-  if (!make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RAg, ka, bpad, size_t(ka) * 4, 32, BM) ||
-      !make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CA, ka, ncols, size_t(ka) * 4, 32, xbox) ||
+  const bool fmaps_ok =
+      half ? make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, RAg, 32, bpad, 64, 32, BM,
+                      CU_TENSOR_MAP_SWIZZLE_64B) &&
+                 make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, CA, 32, ncols, 64, 32, xbox,
+                          CU_TENSOR_MAP_SWIZZLE_64B)
+           : make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RAg, ka, bpad, size_t(ka) * 4, 32,
+                      BM) &&
+                 make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CA, ka, ncols,
+                          size_t(ka) * 4, 32, xbox);
+  if (!fmaps_ok ||
       !make_map(&tm_zhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zhi, ncols, nz, size_t(ldz) * 2, 64, zbox) ||
       !make_map(&tm_zlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Zlo, ncols, nz, size_t(ldz) * 2, 64, zbox))
     return fail(SAP_ERR_DEVICE, "krows_tc: cuTensorMapEncodeTiled failed");

@@ -75,10 +75,15 @@ constexpr int kEpiRegs = 104;
 static_assert(128 * kCtlRegs + 128 * kEpiGroups * kEpiRegs <= kThreads * kLaunchRegs,
               "setmaxnreg budget exceeds the launch allocation");
 
-template <int NZ, int KA>
+// H: the augmented features in fp16 (GEMM1 kind::f16, 64-byte swizzled rows)
+// instead of fp32 (kind::tf32, 128-byte rows): the same 11-bit significands
+// (the features are tf32-rounded splits, exact in fp16), twice the tensor
+// rate and half the bytes per point
+template <int NZ, int KA, bool H = false>
 struct Geometry2 {
-  static constexpr uint32_t a_bytes = BM * KA * 4;             // this CTA's 128 block rows
-  static constexpr uint32_t x_bytes = (NT / 2) * KA * 4;       // this CTA's 64 points
+  static constexpr uint32_t elem = H ? 2 : 4;
+  static constexpr uint32_t a_bytes = BM * KA * elem;          // this CTA's 128 block rows
+  static constexpr uint32_t x_bytes = (NT / 2) * KA * elem;    // this CTA's 64 points
   static constexpr uint32_t z_atom = (NZ / 2) * 128;           // 64 points x nz/2 columns
   static constexpr uint32_t z_bytes = 2 * z_atom;              // 128 points
   static constexpr uint32_t stage_bytes = x_bytes + 2 * z_bytes;
@@ -86,18 +91,24 @@ struct Geometry2 {
   static constexpr uint32_t stages_raw = (kSmemCap - fixed) / stage_bytes;
   static constexpr uint32_t STAGES = stages_raw > 8 ? 8 : stages_raw;
   static constexpr uint32_t smem = fixed + STAGES * stage_bytes;
-  static constexpr bool fits = STAGES >= 3 && NZ % 16 == 0 && NZ >= 16 && kGCol + NZ <= 512;
+  static constexpr bool fits = STAGES >= 3 && NZ % 16 == 0 && NZ >= 16 && kGCol + NZ <= 512 &&
+                              (!H || KA == 32);
 };
 
-template <int FAM, int NZ, int KA>
+// K-major SWIZZLE_64B descriptor (fp16 features: 64-byte rows, 8-row atoms of
+// 512 bytes), start address added to the low bits
+constexpr uint64_t kDescBase64 = (uint64_t(1) << 16) | (uint64_t(512 >> 4) << 32) |
+                                 (uint64_t(1) << 46) | (uint64_t(4) << 61);
+
+template <int FAM, int NZ, int KA, bool H = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     krows_tc2_kernel(const __grid_constant__ CUtensorMap tm_rows,
                      const __grid_constant__ CUtensorMap tm_cols,
                      const __grid_constant__ CUtensorMap tm_zhi,
                      const __grid_constant__ CUtensorMap tm_zlo, const Params p) {
-  using Geo = Geometry2<NZ, KA>;
+  using Geo = Geometry2<NZ, KA, H>;
   constexpr uint32_t STAGES = Geo::STAGES;
-  constexpr int KATOMS = KA / 32;
+  constexpr int KATOMS = H ? 1 : KA / 32;  // 128-byte (fp32) or one 64-byte (fp16) atom
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -207,12 +218,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
     if (cr == 0 && tc::elect_one()) {
-      constexpr uint32_t id1 = tc::idesc(2, 2 * BM, NT);  // tf32, M=256, N=128
+      constexpr uint32_t id1 = tc::idesc(H ? 0 : 2, 2 * BM, NT);  // tf32 / f16, M=256, N=128
       constexpr uint32_t id2 = tc::idesc(0, 2 * BM, NZ);  // f16,  M=256, N=nz
       const uint32_t full0 = tc::smem_u32(full), empty0 = tc::smem_u32(empty);
       const uint32_t sfull0 = tc::smem_u32(s_full), pfull0 = tc::smem_u32(p_full);
       const uint64_t stage_desc0 = kDescBase | (tc::smem_u32(sStage) >> 4);
-      const uint64_t a_desc0 = kDescBase | (tc::smem_u32(sA) >> 4);
+      const uint64_t f_desc0 = (H ? kDescBase64 : kDescBase) | (tc::smem_u32(sStage) >> 4);
+      const uint64_t a_desc0 = (H ? kDescBase64 : kDescBase) | (tc::smem_u32(sA) >> 4);
       uint32_t s1 = 0, ph1 = 0, r1 = 0;    // GEMM1 cursor (one tile ahead)
       uint32_t s2 = 0, r2 = 0, ph2 = 0;    // GEMM2 cursor
       uint32_t sc = 0;
@@ -234,13 +246,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc::fence_after();
           const unsigned long long cw = prof_clock();
           wf += cw - cc;
-          const uint64_t x_desc = stage_desc0 + ((s1 * Geo::stage_bytes) >> 4);
+          const uint64_t x_desc = f_desc0 + ((s1 * Geo::stage_bytes) >> 4);
           const uint32_t d = tmem + r1 * NT;
+          if constexpr (H) {
 #pragma unroll
-          for (int k = 0; k < KA / 8; ++k) {
-            const uint32_t ko = ((k >> 2) * (BM * 128) + (k & 3) * 32) >> 4;
-            const uint32_t kx = ((k >> 2) * ((NT / 2) * 128) + (k & 3) * 32) >> 4;
-            tc::mma_tf32_ss_pair(d, a_desc + ko, x_desc + kx, id1, k > 0);
+            for (int k = 0; k < KA / 16; ++k)  // K = 16 halves (32 bytes) per MMA
+              tc::mma_f16_ss_pair(d, a_desc + 2 * k, x_desc + 2 * k, id1, k > 0);
+          } else {
+#pragma unroll
+            for (int k = 0; k < KA / 8; ++k) {
+              const uint32_t ko = ((k >> 2) * (BM * 128) + (k & 3) * 32) >> 4;
+              const uint32_t kx = ((k >> 2) * ((NT / 2) * 128) + (k & 3) * 32) >> 4;
+              tc::mma_tf32_ss_pair(d, a_desc + ko, x_desc + kx, id1, k > 0);
+            }
           }
           tc::commit_pair(sfull0 + 8 * r1);
           i1 += prof_clock() - cw;
@@ -549,27 +567,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tc::tmem_dealloc_pair(tmem, 512);
 }
 
-template <int FAM, int NZ, int KA>
+template <int FAM, int NZ, int KA, bool H>
 bool launch_tc2_shape(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
                       const CUtensorMap &zl, const Params &p, int grid, cudaStream_t st) {
-  if constexpr (!Geometry2<NZ, KA>::fits) {
+  if constexpr (!Geometry2<NZ, KA, H>::fits) {
     return false;
   } else {
-    constexpr uint32_t smem = Geometry2<NZ, KA>::smem;
-    cudaFuncSetAttribute(krows_tc2_kernel<FAM, NZ, KA>,
+    constexpr uint32_t smem = Geometry2<NZ, KA, H>::smem;
+    cudaFuncSetAttribute(krows_tc2_kernel<FAM, NZ, KA, H>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    krows_tc2_kernel<FAM, NZ, KA><<<grid, kThreads, smem, st>>>(a, c, zh, zl, p);
+    krows_tc2_kernel<FAM, NZ, KA, H><<<grid, kThreads, smem, st>>>(a, c, zh, zl, p);
     return true;
   }
 }
 
+// ka: 32 / 64 fp32 features, or kKaF16 (32 fp16 features, include/sapgp_b200.h)
+constexpr int kKaF16 = SAP_TC_KA_F16;
 template <int FAM>
 bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
                        const CUtensorMap &zl, const Params &p, int nz, int ka, int grid,
                        cudaStream_t st) {
-#define SAP_TC2_KA(NZV)                                                             \
-  return ka == 32 ? launch_tc2_shape<FAM, NZV, 32>(a, c, zh, zl, p, grid, st)      \
-                  : launch_tc2_shape<FAM, NZV, 64>(a, c, zh, zl, p, grid, st);
+#define SAP_TC2_KA(NZV)                                                                   \
+  return ka == 32     ? launch_tc2_shape<FAM, NZV, 32, false>(a, c, zh, zl, p, grid, st)  \
+         : ka == 64   ? launch_tc2_shape<FAM, NZV, 64, false>(a, c, zh, zl, p, grid, st)  \
+         : ka == kKaF16 ? launch_tc2_shape<FAM, NZV, 32, true>(a, c, zh, zl, p, grid, st) \
+                        : false;
   switch (nz) {
     case 16: SAP_TC2_KA(16)
     case 32: SAP_TC2_KA(32)
@@ -585,9 +607,12 @@ bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtenso
 }
 
 inline bool tc2_fits(int nz, int ka) {
+  const bool h = ka == kKaF16;
+  if (h) ka = 32;
   if (nz % 16 || nz < 16 || kGCol + nz > 512 || (ka != 32 && ka != 64)) return false;
-  const uint32_t stage = (NT / 2) * ka * 4 + 2 * 2 * (nz / 2) * 128;
-  const uint32_t fixed = 1024 + 2 * BM * ka * 4 + 512;
+  const uint32_t elem = h ? 2 : 4;
+  const uint32_t stage = (NT / 2) * ka * elem + 2 * 2 * (nz / 2) * 128;
+  const uint32_t fixed = 1024 + 2 * BM * ka * elem + 512;
   return (kSmemCap - fixed) / stage >= 3;
 }
 

@@ -22,6 +22,7 @@ tensors.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -134,6 +135,11 @@ def krows_times(spec, cols, Rs, rsq, row_ids, R, out, col_ids=None, col_base=0, 
     return out
 
 
+_LOG2E = 1.4426950408889634
+# c_fam of the augmented features (krows_tc.cu, sap_tc_points): z = x sqrt(c) / l
+_CFAM = {"rbf": 0.5 * _LOG2E, "matern32": 3.0 * _LOG2E ** 2, "matern52": 5.0 * _LOG2E ** 2}
+
+
 class TcPoints:
     """Augmented features of the tensor-core path (krows_tc.cu): row form RA
     for every point (rows are gathered per block) and column form CA for the
@@ -149,6 +155,7 @@ class TcPoints:
         if feats > 64:
             raise ContractError(f"tensor-core path supports d <= 19 (got d={d})")
         inv = torch.as_tensor(np.broadcast_to(1.0 / spec.lengthscales, (d,)).copy(), device=device)
+        self._ls, self._family = spec.lengthscales, spec.family
         self.RA = torch.empty((max(n, 1), self.ka), dtype=torch.float32, device=device)
         self.CA = torch.empty((max(hi - lo, 1), self.ka), dtype=torch.float32, device=device)
         with torch.cuda.device(device):
@@ -159,23 +166,57 @@ class TcPoints:
                          self.ka, None, nat.ptr(self.CA), nat.stream_handle())
         self.lo, self.hi, self.n, self.d, self.device = lo, hi, n, d, device
         self.code = spec.code
+        # fp16 features (GEMM1 kind::f16 at twice the tf32 rate, half the bytes):
+        # the features are tf32-rounded splits, so the fp16 copy is exact while
+        # every magnitude stays inside fp16's range (|z|^2 < 2^14 leaves room
+        # for the -2 z column form); SAP_TC_F16=0 keeps fp32
+        self.half = False
+        if self.ka == 32 and os.environ.get("SAP_TC_F16", "1") == "1":
+            zmax2 = _CFAM[spec.family] * float(((Xd * inv) ** 2).sum(1).max())
+            self.half = zmax2 < 2.0 ** 14
+        self.ka_code = nat.SAP_TC_KA_F16 if self.half else self.ka
+        self.dtype = torch.float16 if self.half else torch.float32
+        if self.half:
+            self.CA = self.CA.half()
+
+    def fits_half(self, Xs):
+        """True when external points (test points) keep their features in fp16 range."""
+        if not self.half:
+            return True
+        Xs = torch.as_tensor(Xs, dtype=torch.float64, device=self.device)
+        inv = torch.as_tensor(np.broadcast_to(1.0 / self._ls, (self.d,)).copy(),
+                              device=self.device)
+        return _CFAM[self._family] * float(((Xs * inv) ** 2).sum(1).max()) < 2.0 ** 14
+
+    def _scratch(self, rows):
+        # fp32 staging for the gathers when the kernel reads fp16 features: a
+        # fresh (stream-ordered, caching-allocator) buffer per call, since the
+        # lookahead's producer threads gather concurrently
+        return torch.empty((rows, self.ka), dtype=torch.float32, device=self.device)
 
     def gather_cols(self, idx_dev, out=None):
-        """Column-form features of the points idx (any ids, not only this shard)."""
+        """Column-form features of the points idx (any ids, not only this shard),
+        in the kernel's feature dtype."""
         b = idx_dev.numel()
         if out is None:
-            out = torch.empty((b, self.ka), dtype=torch.float32, device=self.device)
+            out = torch.empty((b, self.ka), dtype=self.dtype, device=self.device)
+        dst = self._scratch(out.shape[0]) if self.half else out
         nat.call("sap_tc_gather_cols", nat.ptr(self.RA), self.ka, self.d, self.code,
-                 nat.ptr(idx_dev), b, out.shape[0], nat.ptr(out), nat.stream_handle())
+                 nat.ptr(idx_dev), b, dst.shape[0], nat.ptr(dst), nat.stream_handle())
+        if self.half:
+            out.copy_(dst)
         return out
 
     def gather_rows(self, idx_dev, out=None):
         b = idx_dev.numel()
         bpad = (b + 255) // 256 * 256  # whole 256-row tiles of the CTA-pair kernel
         if out is None:
-            out = torch.empty((bpad, self.ka), dtype=torch.float32, device=self.device)
+            out = torch.empty((bpad, self.ka), dtype=self.dtype, device=self.device)
+        dst = self._scratch(out.shape[0]) if self.half else out
         nat.call("sap_tc_gather_rows", nat.ptr(self.RA), self.ka, nat.ptr(idx_dev), b, bpad,
-                 nat.ptr(out), nat.stream_handle())
+                 nat.ptr(dst), nat.stream_handle())
+        if self.half:
+            out.copy_(dst)
         return out
 
 
@@ -215,7 +256,9 @@ def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False, co
     need = nat.load().sap_krows_tc_workspace(b, zop.m, ncols)
     if ws is None or ws.numel() * 4 < need:
         ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=tcp.device)
-    nat.call("sap_krows_tc", nat.ptr(CA), ncols, tcp.ka, nat.ptr(RAg), RAg.shape[0],
+    if RAg.dtype != tcp.dtype or CA.dtype != tcp.dtype:
+        raise ContractError("tensor-core features must be in the point set's dtype")
+    nat.call("sap_krows_tc", nat.ptr(CA), ncols, tcp.ka_code, nat.ptr(RAg), RAg.shape[0],
              nat.ptr(row_ids), b, col_base, nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz,
              nat.ptr(zop.scale), zop.m, spec.code, spec.variance, nat.ptr(out), out.stride(0),
              int(accumulate), nat.ptr(ws), ws.numel() * 4, nat.stream_handle())
@@ -403,7 +446,7 @@ class KernelOracle:
         Rcm = to_colmajor(W, self.n, self.device)
         t, m = star.n, Rcm.shape[0]
         out = torch.empty((t, m), dtype=torch.float32, device=self.device)
-        if self.use_tc(m) and t >= 16:
+        if self.use_tc(m) and t >= 16 and self.tc_points().fits_half(Xstar):
             # test points as the rows of the tensor-core kernel: their row-form
             # features, zero padded to whole 256-row tiles; no row ids, so no
             # diagonal rule (kernels.py:161-176)
@@ -416,6 +459,7 @@ class KernelOracle:
                                                   (self.d,)).copy(), device=self.device)
             nat.call("sap_tc_points", nat.ptr(Xs64), t, self.d, nat.ptr(inv), self.spec.code,
                      tcp.ka, nat.ptr(RAs), None, nat.stream_handle())
+            RAs = RAs.to(tcp.dtype)
             zop = ZOperand(m, self.n, self.device).fill(Rcm)
             krows_tc(self.spec, tcp, RAs, t, None, zop, out)
             return _finish(out, like_np, vector)

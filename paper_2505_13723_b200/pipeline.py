@@ -60,7 +60,7 @@ class IterPlan:
 
 
 class _Slot:
-    def __init__(self, L, b, r, ldx, dev, ka=0):
+    def __init__(self, L, b, r, ldx, dev, ka=0, fdtype=torch.float32):
         f32, f64, i64 = torch.float32, torch.float64, torch.int64
         self.block_dev = torch.empty((L, b), dtype=i64, device=dev)
         self.loc_dev = torch.empty((L, b), dtype=i64, device=dev)
@@ -77,7 +77,7 @@ class _Slot:
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
         bpad = (b + 255) // 256 * 256
-        self.RAg = torch.empty((L, bpad, ka), dtype=f32, device=dev) if ka else None
+        self.RAg = torch.empty((L, bpad, ka), dtype=fdtype, device=dev) if ka else None
         pin = torch.cuda.is_available()
         self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
         # Omega_t is drawn on the GPU from the omega stream's PCG64 state
@@ -136,7 +136,8 @@ class Lookahead:
             self.sides = [torch.cuda.current_stream(dev)] * 3
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
-        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka) for _ in range(3)]
+        fdt = tcp.dtype if tcp is not None else torch.float32
+        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka, fdt) for _ in range(3)]
         # per-slot scratch of the tensor-core sketch (used one plan at a time by
         # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
@@ -147,7 +148,7 @@ class Lookahead:
             need = K.nat.load().sap_krows_tc_workspace(b, self.r, b)
             for slot in self.slots:
                 slot.sk_zop = K.ZOperand(self.r, b, dev)
-                slot.sk_cols = torch.empty((b, ka), dtype=torch.float32, device=dev)
+                slot.sk_cols = torch.empty((b, ka), dtype=fdt, device=dev)
                 slot.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
         # batch k covers iterations [bounds[k], bounds[k+1])
         self.bounds = [0]

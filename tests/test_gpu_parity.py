@@ -233,3 +233,25 @@ def test_cross_matmul_tensor_path_matches_oracle(fam):
     got = o.cross_matmul(Xs, W)
     ref = orc.cross_matmul(orc.Points(fam, ls, 1.3, X), ls, Xs, W)
     assert rel(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("fam", FAMILIES)
+def test_fp16_and_fp32_feature_paths_agree(fam, monkeypatch):
+    """The distance GEMM on fp16 features (kind::f16, the default when the
+    point norms fit) and on fp32 features (kind::tf32, SAP_TC_F16=0) give the
+    same block product to fp32-level accuracy, and both match the oracle."""
+    rng = np.random.default_rng(11)
+    n, d, b, m = 20000, 9, 512, 65
+    X = rng.standard_normal((n, d))
+    ls = np.full(d, 3.0)
+    W = rng.standard_normal((n, m))
+    B = np.sort(rng.choice(n, b, replace=False))
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SAP_TC_F16", flag)
+        o = sap.KernelOracle(sap.KernelSpec(fam, ls, 1.0), X, 1e-2)
+        assert o.tc_points().half == (flag == "1")
+        out[flag] = sap.col_dist_matmul(o, W, B)
+    ref = orc.col_dist_matmul(orc.Points(fam, ls, 1.0, X), W, B, workers=8)
+    assert rel(out["1"], ref) < 2e-5 and rel(out["0"], ref) < 2e-5
+    assert rel(out["1"], out["0"]) < 2e-5
