@@ -51,6 +51,9 @@ extern "C" {
 
 enum { SAP_OK = 0, SAP_ERR_CONTRACT = 1, SAP_ERR_NUMERICAL = 2, SAP_ERR_DEVICE = 3 };
 enum { SAP_RBF = 0, SAP_MATERN32 = 1, SAP_MATERN52 = 2 };
+/* "family" of the random-feature prior product (gp.py:49-114): the kernel
+ * value is cos(x . F_k + p_k) instead of k(x, y); sap_krows_tc only */
+enum { SAP_COSINE = 3 };
 #define SAP_TC_KA_F16 48
 
 int sap_abi_version(void);
@@ -200,6 +203,19 @@ int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t
                  const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
                  double variance, float *out, int64_t ldo, int accumulate, void *ws,
                  size_t ws_bytes, void *stream);
+
+/*
+ * Augmented features of the random-feature prior product (gp.py:49-114):
+ * rows (points X, n x d fp64) RA[n][32] = [xh, xh, xl, 1, 1, 0...] and columns
+ * (frequencies F, q x d fp64, phases p) CA[q][32] = [Fh, Fl, Fh, ph, pl, 0...]
+ * (tf32-rounded splits), so the tensor-core GEMM gives x.F_k + p_k to ~2^-21
+ * relative. Either output may be NULL; d <= 9.
+ * sap_krows_tc(..., family = SAP_COSINE, variance = sqrt(2 var / q), ...) then
+ * computes out = variance * cos(X F^T + p) Z, Z = theta (q x s) -- phi(X) theta
+ * without materialising phi.
+ */
+int sap_cos_features(const double *X, int64_t n, int d, const double *F, const double *phase,
+                     int64_t q, float *RA, float *CA, void *stream);
 
 /*
  * SDD step (solvers.py:463-516, the stochastic-dual-descent baseline on the

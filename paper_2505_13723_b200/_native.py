@@ -57,6 +57,7 @@ SIGNATURES = {
     "sap_colabsmax": (_I, [_P, _I64, _I64, _I, _P, _P]),
     "sap_krows_tc_workspace": (_SZ, [_I64, _I, _I64]),
     "sap_tc_supported": (_I, [_I, _I]),
+    "sap_cos_features": (_I, [_P, _I64, _I, _P, _P, _I64, _P, _P, _P]),
     "sap_sdd_update": (_I, [_P, _P, _P, _I64, _I64, _I, _P, _I64, _P, _I64, _D, _D, _D, _P, _P,
                             _P]),
     "sap_normal_workspace": (_SZ, [_I64, _I]),

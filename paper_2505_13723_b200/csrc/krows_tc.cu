@@ -31,6 +31,8 @@ bool launch_tc2_m32(const CUtensorMap &, const CUtensorMap &, const CUtensorMap 
                     const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
 bool launch_tc2_m52(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
                     const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
+bool launch_tc2_cos(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
+                    const CUtensorMap &, const Params &, int, int, int, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // augmented features for the 3-term tf32 distance GEMM
@@ -90,6 +92,35 @@ __global__ void build_aug_kernel(const double *X, int64_t n, int d, const double
   for (int k = used; k < ka; ++k) {
     if (ra) ra[k] = 0.0f;
     if (ca) ca[k] = 0.0f;
+  }
+}
+
+// random-feature rows / columns (sap_cos_features): x.F + p from a 3-term split
+__global__ void cos_features_kernel(const double *X, int64_t n, int d, const double *F,
+                                    const double *phase, int64_t q, float *RA, float *CA) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  constexpr int ka = 32;
+  if (RA && j < n) {
+    float *ra = RA + j * ka;
+    for (int k = 0; k < d; ++k) {
+      const double x = X[j * d + k];
+      const float h = tf32_trunc(float(x));
+      ra[k] = h; ra[d + k] = h; ra[2 * d + k] = tf32_round(float(x - double(h)));
+    }
+    ra[3 * d] = 1.0f; ra[3 * d + 1] = 1.0f;
+    for (int k = 3 * d + 2; k < ka; ++k) ra[k] = 0.0f;
+  }
+  if (CA && j < q) {
+    float *ca = CA + j * ka;
+    for (int k = 0; k < d; ++k) {
+      const double f = F[j * d + k];
+      const float h = tf32_trunc(float(f));
+      ca[k] = h; ca[d + k] = tf32_round(float(f - double(h))); ca[2 * d + k] = h;
+    }
+    const double p = phase[j];
+    const float ph = tf32_trunc(float(p));
+    ca[3 * d] = ph; ca[3 * d + 1] = tf32_round(float(p - double(ph)));
+    for (int k = 3 * d + 2; k < ka; ++k) ca[k] = 0.0f;
   }
 }
 
@@ -300,6 +331,17 @@ int sap_tc_points(const double *X, int64_t n, int d, const double *inv_ls, int f
   return check_launch("build_aug_kernel");
 }
 
+int sap_cos_features(const double *X, int64_t n, int d, const double *F, const double *phase,
+                     int64_t q, float *RA, float *CA, void *stream) {
+  if (n < 0 || q < 0 || d < 1 || 3 * d + 2 > 32)
+    return fail(SAP_ERR_CONTRACT, "cos_features: d=%d outside the tensor-core path (d <= 9)", d);
+  const int64_t rows = std::max(RA ? n : 0, CA ? q : 0);
+  if (rows == 0) return SAP_OK;
+  cos_features_kernel<<<unsigned((rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      X, n, d, F, phase, q, RA, CA);
+  return check_launch("cos_features_kernel");
+}
+
 int sap_tc_gather_rows(const float *RA, int ka, const int64_t *idx, int64_t b, int64_t bpad,
                        float *out, void *stream) {
   if (b <= 0 || bpad < b) return fail(SAP_ERR_CONTRACT, "tc_gather_rows: bad shape");
@@ -466,6 +508,9 @@ int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t
   else if (family == SAP_MATERN52)
     launched = pair ? launch_tc2_m52(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st)
                     : launch_tc_m52(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
+  else if (family == SAP_COSINE)
+    launched = pair && ka == 32 && !row_ids &&
+               launch_tc2_cos(tm_rows, tm_cols, tm_zhi, tm_zlo, p, nz, ka, grid, st);
   else
     return fail(SAP_ERR_CONTRACT, "krows_tc: unknown family %d", family);
   if (!launched) return fail(SAP_ERR_CONTRACT, "krows_tc: shape nz=%d ka=%d unsupported", nz, ka);

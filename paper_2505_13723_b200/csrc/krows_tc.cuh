@@ -128,6 +128,14 @@ template <int FAM, bool POLY = false>
 __device__ __forceinline__ float pvalue(float s) {
   if constexpr (FAM == SAP_RBF) {
     return POLY ? ex2_poly(s) : ex2_approx(s);
+  } else if constexpr (FAM == SAP_COSINE) {
+    // random-feature prior: P = 2^14 cos(s), s = x.F + p; reduced to
+    // [-pi, pi] first (cos.approx is accurate to ~2^-21 there)
+    const float r = s * 0.15915494309189535f;
+    const float f = r - rintf(r);
+    float c;
+    asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(f * 6.283185307179586f));
+    return kPScale * c;
   } else {
     // the 2^14 scale rides on the polynomial, so ex2 takes -t directly;
     // t = s * rsqrt(s) with s floored at 1e-30 (which also clamps negative

@@ -501,3 +501,39 @@ def block_block(oracle, block):
 
 def default_lengthscales(d):
     return np.full(d, math.sqrt(d))
+
+
+SAP_COSINE = 3  # include/sapgp_b200.h: the random-feature "family" of sap_krows_tc
+
+
+def cos_features_times(freq, phases, variance, X, theta, device):
+    """phi(X) @ theta with phi = sqrt(2 var / q) cos(X F^T + p) (gp.py:49-114) on
+    the tensor-core kernel: rows = points, columns = the q features, Z = theta,
+    the epilogue evaluating cos instead of a covariance (never materialising
+    phi). Returns an (n x s) float32 device tensor, or None when the shape is
+    outside the tensor path (d > 9, s > 128)."""
+    dev = _device(device)
+    Xd = torch.as_tensor(X if torch.is_tensor(X) else np.asarray(X, dtype=np.float64),
+                         dtype=torch.float64).to(dev).contiguous()
+    F = torch.as_tensor(np.asarray(freq, dtype=np.float64), device=dev).contiguous()
+    P = torch.as_tensor(np.asarray(phases, dtype=np.float64), device=dev).contiguous()
+    T = theta if torch.is_tensor(theta) else np.asarray(theta, dtype=np.float64)
+    n, d = Xd.shape
+    q, s = F.shape[0], T.shape[1]
+    if d > 9 or s > 128 or n < 1 or q < 1:
+        return None
+    bpad = (n + 255) // 256 * 256
+    RA = torch.zeros((bpad, 32), dtype=torch.float32, device=dev)
+    CA = torch.empty((q, 32), dtype=torch.float32, device=dev)
+    with torch.cuda.device(dev):
+        nat.call("sap_cos_features", nat.ptr(Xd), n, d, nat.ptr(F), nat.ptr(P), q, nat.ptr(RA),
+                 nat.ptr(CA), nat.stream_handle())
+        zop = ZOperand(s, q, dev).fill(to_colmajor(T, q, dev))
+        out = torch.empty((n, s), dtype=torch.float32, device=dev)
+        need = nat.load().sap_krows_tc_workspace(n, s, q)
+        ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
+        nat.call("sap_krows_tc", nat.ptr(CA), q, 32, nat.ptr(RA), bpad, None, n, 0,
+                 nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz, nat.ptr(zop.scale), s,
+                 SAP_COSINE, math.sqrt(2.0 * variance / q), nat.ptr(out), out.stride(0), 0,
+                 nat.ptr(ws), ws.numel() * 4, nat.stream_handle())
+    return out

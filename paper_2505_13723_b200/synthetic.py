@@ -73,7 +73,15 @@ def feature_map(family, lengthscales, q, rng):
 
 def features_times(freq, phases, variance, X, theta, device=None, chunk=65536):
     """phi(X) @ theta with phi = sqrt(2 var / q) cos(X F^T + p), never
-    materialising phi for all rows (gp.py:65-70)."""
+    materialising phi for all rows (gp.py:65-70): on a CUDA device the fused
+    tensor-core product (kernels.cos_features_times), else -- shapes outside
+    it, or host-only data generation -- chunked fp64 torch."""
+    if device is not None and torch.device(device).type == "cuda":
+        from .kernels import cos_features_times
+        out = cos_features_times(freq, phases, variance, np.asarray(X, dtype=np.float64),
+                                 np.asarray(theta, dtype=np.float64), device)
+        if out is not None:
+            return out.double().cpu().numpy()
     dev = torch.device(device) if device is not None else torch.device("cpu")
     F = torch.as_tensor(freq, dtype=torch.float64, device=dev)
     P = torch.as_tensor(phases, dtype=torch.float64, device=dev)

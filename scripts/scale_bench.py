@@ -61,9 +61,19 @@ def timed(fn, reps=3):
 res = {"workload": f"synthetic {a.family} GP n={n} d={d} m={m}", "gpu": torch.cuda.get_device_name(0)}
 t0 = time.perf_counter()
 prob = synthetic.make_problem(n, d, a.family, m, seed=0, lam=1e-2, device=dev)
-res["prior_rhs"] = {"seconds_host_timed": time.perf_counter() - t0,
+res["prior_rhs"] = {"make_problem_seconds_host_timed": time.perf_counter() - t0,
                     "what": "make_problem: phi(X) theta for n + 10^4 points, q=2048 cosine "
-                            "features, 65 columns (torch fp64, chunked), plus host draws"}
+                            "features, 65 columns (fused tensor-core product), plus the host "
+                            "numpy draws (X, noise, zeta: n x 64 normals)"}
+from paper_2505_13723_b200.kernels import cos_features_times  # noqa: E402
+from paper_2505_13723_b200.synthetic import feature_map  # noqa: E402
+from paper_2505_13723_b200.rng import substream  # noqa: E402
+_fr, _ph = feature_map(a.family, np.full(d, np.sqrt(d)), 2048, substream(0, "features"))
+_th = np.random.default_rng(1).standard_normal((2048, m))
+_Xd = torch.as_tensor(prob.X, device=dev)
+res["prior_rhs"]["fused_product_ms"] = timed(
+    lambda: cos_features_times(_fr, _ph, 1.0, _Xd, _th, dev), reps=3)
+res["prior_rhs"]["entries_per_s"] = n * 2048 / (res["prior_rhs"]["fused_product_ms"] * 1e-3)
 spec = prob.spec()
 o = sap.KernelOracle(spec, prob.X, prob.lam, device=dev)
 

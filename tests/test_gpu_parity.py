@@ -255,3 +255,20 @@ def test_fp16_and_fp32_feature_paths_agree(fam, monkeypatch):
     ref = orc.col_dist_matmul(orc.Points(fam, ls, 1.0, X), W, B, workers=8)
     assert rel(out["1"], ref) < 2e-5 and rel(out["0"], ref) < 2e-5
     assert rel(out["1"], out["0"]) < 2e-5
+
+
+@pytest.mark.parametrize("fam", FAMILIES)
+def test_random_feature_prior_on_tensor_cores(fam):
+    """phi(X) theta for the pathwise prior (gp.py:49-114) on the fused
+    tensor-core product (cosine epilogue) against the reference's dense fp64
+    formula, scale * cos(X F^T + p) @ theta."""
+    rng = np.random.default_rng(3)
+    n, d, q, s = 6000, 9, 2048, 65
+    X = rng.standard_normal((n, d))
+    rfm = sap.RandomFeatureMap.sample(sap.KernelSpec(fam, np.full(d, 3.0), 1.3), q, 5)
+    theta = rng.standard_normal((q, s))
+    got = rfm.times(X, theta, device="cuda")
+    ref = np.sqrt(2.0 * 1.3 / q) * np.cos(X @ rfm.frequencies.T + rfm.phases) @ theta
+    assert rel(got, ref) < 5e-5
+    vec = rfm.times(X[:100], theta[:, 0], device="cuda")
+    assert vec.shape == (100,) and rel(vec, ref[:100, 0]) < 5e-5
