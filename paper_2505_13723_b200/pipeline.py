@@ -11,8 +11,8 @@ block-row product and the update depends only on (seed, t) and X:
     eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
                                    10, substream(seed, "power", t)) :389-396
 
-so they are produced in batches by two host producer threads, up to two
-batches ahead of the block-row products that consume them; their GPU work is
+so they are produced in batches by ``depth`` (default 3) host producer
+threads, up to ``depth`` batches ahead of the block-row products that consume them; their GPU work is
 enqueued in order on the solver's stream (see Lookahead.__init__).
 Batch sizes ramp 1, 2, 4, ... up to ``L = config.lookahead`` so the first
 iteration waits for one plan only, not for a full batch. Per batch there is one device->host
@@ -73,7 +73,9 @@ class _Slot:
         self.v0 = torch.empty((L, b), dtype=f64, device=dev)
         # K_BB in fp32: the values the tile kernel computes (fp32 arithmetic),
         # streamed once per power step by sap_power_stepsize
-        self.Kbb = torch.empty((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
+        # zeroed: the power kernel reads rows in 16-byte chunks through the pad
+        # columns (times a zero w); never-written pad bits must not be NaN
+        self.Kbb = torch.zeros((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
         bpad = (b + 255) // 256 * 256
@@ -116,8 +118,15 @@ class Lookahead:
                  tcp=None):
         self.o, self.shard, self.seed = oracle, shard, seed
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
-        # three slots of L fp32 b x b blocks: keep them under ~3 GB
-        cap = max(1, int(3e9 // (3 * 4 * b * b)))
+        # batches produced concurrently (one producer thread each, depth + 1
+        # slots): a producer spends most of a batch waiting -- for its sketch,
+        # queued behind the block products already enqueued, and on the host
+        # factorisation -- so two producers left the solver host-bound at ~1.43
+        # ms per RBF iteration against 1.25 with four (scripts/host_bound.py,
+        # config 3); SAP_LOOKAHEAD_DEPTH overrides
+        self.depth = max(2, int(os.environ.get("SAP_LOOKAHEAD_DEPTH", "4")))
+        # depth + 1 slots of L fp32 b x b blocks: keep them under ~4 GB
+        cap = max(1, int(4e9 // ((self.depth + 1) * 4 * b * b)))
         self.total, self.L = total, max(1, min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
@@ -131,13 +140,14 @@ class Lookahead:
         # SAP_SIDE_STREAM=1 selects the side streams for experiments.
         self.main = torch.cuda.current_stream(dev)
         if os.environ.get("SAP_SIDE_STREAM", "0") == "1":
-            self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(3)]
+            self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(self.depth + 1)]
         else:
-            self.sides = [torch.cuda.current_stream(dev)] * 3
+            self.sides = [torch.cuda.current_stream(dev)] * (self.depth + 1)
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
         fdt = tcp.dtype if tcp is not None else torch.float32
-        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka, fdt) for _ in range(3)]
+        self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka, fdt)
+                      for _ in range(self.depth + 1)]
         # per-slot scratch of the tensor-core sketch (used one plan at a time by
         # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
@@ -156,10 +166,10 @@ class Lookahead:
         while self.bounds[-1] < total:
             self.bounds.append(min(total, self.bounds[-1] + c))
             c = min(2 * c, self.L)
-        # two producers: a batch's production (host RNG -> sketch on the GPU ->
+        # depth producers: a batch's production (host RNG -> sketch on the GPU ->
         # host factorisation -> power iteration) takes longer than consuming
-        # one, so two batches are produced concurrently (slots k, k+1 mod 3)
-        self.pool = ThreadPoolExecutor(max_workers=2, thread_name_prefix="sap-lookahead")
+        # one, so depth batches are produced concurrently (slots k mod depth+1)
+        self.pool = ThreadPoolExecutor(max_workers=self.depth, thread_name_prefix="sap-lookahead")
         # host workers for the per-iteration numpy RNG and r x r LAPACK work (both
         # release the GIL in their kernels); sized to leave cores for the main thread
         try:
@@ -186,13 +196,14 @@ class Lookahead:
         self.cur = None
         self.k = -1  # batch currently consumed
         self.futs = {}
-        for k in range(min(2, len(self.bounds) - 1)):
+        for k in range(min(self.depth, len(self.bounds) - 1)):
             self._submit(k)
 
     def _submit(self, k):
         t0, t1 = self.bounds[k], self.bounds[k + 1]
-        self.futs[k] = self.pool.submit(self._produce, self.slots[k % 3], t0, t1 - t0,
-                                        self.sides[k % 3])
+        ns = len(self.slots)
+        self.futs[k] = self.pool.submit(self._produce, self.slots[k % ns], t0, t1 - t0,
+                                        self.sides[k % ns])
 
     def close(self):
         self.pool.shutdown(wait=True)
@@ -214,8 +225,8 @@ class Lookahead:
             cur = self.futs.pop(self.k).result()
             main.wait_event(cur.ready)
             self.cur = cur
-            if self.k + 2 < len(self.bounds) - 1:
-                self._submit(self.k + 2)
+            if self.k + self.depth < len(self.bounds) - 1:
+                self._submit(self.k + self.depth)
         i = t - cur.t0
         s = cur.slot
         ev, h_eta = cur.eta_ready, s.h_eta

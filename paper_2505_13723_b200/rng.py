@@ -69,6 +69,7 @@ class DeviceNormals:
         nbytes = lib.sap_normal_workspace(self.count, self.nstreams)
         self.ws = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=device)
         assert lib.sap_normal_status(nat.ptr(self.ws)) == self.ws.data_ptr()
+        self.ws[0] = 0  # status word: 0 until a fill reports otherwise
 
     def fill(self, states, out, nstreams=None):
         ns = self.nstreams if nstreams is None else int(nstreams)
