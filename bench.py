@@ -41,7 +41,9 @@ for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at this
 # config, from the committed ncu capture (profiles/); re-capture when the kernel changes.
-TRAFFIC_PER_LAUNCH = 508_532_736  # profiles/r01_krows_tc2_m32_ncu_summary.txt (488.02 MB read + 20.51 MB write)
+# dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at config 3
+# (profiles/r01e_krows_tc2_*_ncu_summary.txt, ncu --set full)
+TRAFFIC_PER_LAUNCH = {"matern32": 416_395_008 + 21_179_392, "rbf": 416_449_280 + 19_812_352}
 
 CONFIG = dict(n=1_000_000, d=9, family="matern32", b=2000, m=65, r=100, lam=1e-2, seed=0)
 METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target RMSE"
@@ -331,7 +333,8 @@ def run_b200(args):
         "kernel_entries_per_s": entries / (ms_step * 1e-3),
         "krows_ms": kmean,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak,
-                     "unit": "TFLOP/s", "frac": achieved / bf16_peak, "traffic": TRAFFIC_PER_LAUNCH,
+                     "unit": "TFLOP/s", "frac": achieved / bf16_peak,
+                     "traffic": TRAFFIC_PER_LAUNCH.get(args.family) if eng.use_tc else None,
                      "kernel": kernel_name,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst), of measured",
                      "algorithmic": f"{b}*{n_local}*2*({d}+{m}) flop per launch "
