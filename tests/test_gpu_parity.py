@@ -272,3 +272,27 @@ def test_random_feature_prior_on_tensor_cores(fam):
     assert rel(got, ref) < 5e-5
     vec = rfm.times(X[:100], theta[:, 0], device="cuda")
     assert vec.shape == (100,) and rel(vec, ref[:100, 0]) < 5e-5
+
+
+@pytest.mark.parametrize("n,d,b,m", [(300, 9, 16, 128), (5000, 9, 513, 113), (4097, 10, 256, 65),
+                                     (129, 2, 129, 17), (20000, 19, 700, 1)])
+def test_tensor_core_edge_shapes(n, d, b, m):
+    """Tensor-core path at its shape limits: the smallest block it takes (16 rows),
+    nz = 128 (TMEM full), ragged column tiles, d = 10 / 19 (fp32 features, ka
+    = 64), b = n, m = 1; the block holds the first and last points; exact
+    duplicate points (distance 0 off the diagonal: Matern's cusp) included."""
+    rng = np.random.default_rng(n * 7 + m)
+    X = rng.standard_normal((n, d))
+    X[n // 2] = X[1]  # an exact duplicate pair
+    ls = rng.uniform(0.8, 2.5, d)
+    B = np.sort(np.union1d(rng.choice(n, b - 2, replace=False), [0, n - 1]))[:b]
+    if 1 not in B:
+        B[1] = 1
+        B = np.sort(np.unique(np.concatenate([B, [n // 2]])))
+    W = rng.standard_normal((n, m))
+    for fam in FAMILIES:
+        o = sap.KernelOracle(sap.KernelSpec(fam, ls, 0.9), X, 0.1)
+        assert o.use_tc(m)
+        got = sap.col_dist_matmul(o, W, B)
+        ref = orc.col_dist_matmul(orc.Points(fam, ls, 0.9, X), W, B, workers=8)
+        assert rel(got, ref) < TOL_BLOCK, (fam, rel(got, ref))
