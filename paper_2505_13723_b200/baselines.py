@@ -17,8 +17,8 @@ columns = all points). What is new here:
 
 Deviations: block products fp32-accurate (split-precision tensor cores, as
 everywhere in this package); SDD state fp32 (reference fp64); the PCG
-Omega draw is numpy's host draw (bit-exact; (n, r) exceeds the device
-sampler's per-stream limit at scale).
+Omega draw runs on the GPU at scale (numpy-exact but for 1-ulp ziggurat-tail
+values, rng.py).
 """
 
 from __future__ import annotations
@@ -35,7 +35,7 @@ from .errors import ConfigError, ContractError, NumericalError
 from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
 from .parallel import allreduce_sum_, current_shard, gather_rows
 from .randnla import rand_nystrom_retry, woodbury_core
-from .rng import block_hash, substream, uniform_block
+from .rng import block_hash, standard_normal, substream, uniform_block
 
 SDD_MOMENTUM = 0.9          # solvers.py:25
 DIVERGENCE_FACTOR = 1e6     # solvers.py:24
@@ -226,8 +226,11 @@ def sdd_solve(oracle, Y, config, pool=None, on_iterate=None):
     return SolveResult(est[:, 0] if eng.vector else est, trace, diverged, done, done * b / n)
 
 
-def _omega(seed, n, rank):
-    return substream(seed, "omega").standard_normal((n, rank))
+def _omega(seed, n, rank, device=None):
+    """substream(seed, "omega").standard_normal((n, r)) (solvers.py:538), on the
+    GPU at scale (rng.standard_normal)."""
+    z = standard_normal(substream(seed, "omega"), (n, rank), device)
+    return z.cpu().numpy() if torch.is_tensor(z) else z
 
 
 def pcg_solve(oracle, Y, config, pool=None, on_iterate=None):
@@ -250,7 +253,7 @@ def pcg_solve(oracle, Y, config, pool=None, on_iterate=None):
         raise ConfigError("pcg rank outside [0, n]")
     f64 = torch.float64
     if rank > 0:
-        omega = _omega(config.seed, n, rank)
+        omega = _omega(config.seed, n, rank, dev)
         sketch = oracle.matmul(omega)
         factor = rand_nystrom_retry(sketch, omega, rank)
         rho = float(factor.S[-1]) + lam

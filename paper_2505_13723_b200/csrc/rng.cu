@@ -116,30 +116,33 @@ __global__ void raw_kernel(const uint64_t *states, int64_t L, uint64_t *R) {
   }
 }
 
-__global__ void __launch_bounds__(256) classify_kernel(const uint64_t *Rall, int64_t L,
-                                                      double *valall, int *codeall) {
-  // the tables are indexed by a per-thread layer: gathered from shared memory
-  // (divergent __constant__ reads serialise)
-  __shared__ uint64_t ki[256];
-  __shared__ double wi[256], fi[256];
-  ki[threadIdx.x] = zig::ki[threadIdx.x];
-  wi[threadIdx.x] = zig::wi[threadIdx.x];
-  fi[threadIdx.x] = zig::fi[threadIdx.x];
-  __syncthreads();
-  const int s = blockIdx.y;
-  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= L) return;
-  const uint64_t *R = Rall + s * L;
+// The ziggurat tables, gathered into shared memory by every kernel that
+// indexes them per thread (divergent __constant__ reads serialise).
+struct ZigTables {
+  uint64_t ki[256];
+  double wi[256], fi[256];
+};
+__device__ __forceinline__ void load_tables(ZigTables &t) {
+  for (int k = threadIdx.x; k < 256; k += blockDim.x) {
+    t.ki[k] = zig::ki[k];
+    t.wi[k] = zig::wi[k];
+    t.fi[k] = zig::fi[k];
+  }
+}
+
+// The draw that would start at raw word p: its value and code (words consumed,
+// bit 30 = emits; 0 = runs past the L generated words).
+__device__ __forceinline__ void draw_at(const uint64_t *R, int64_t L, int64_t p,
+                                        const ZigTables &t, double &val, int &code) {
   uint64_t r = R[p];
   const int idx = int(r & 0xff);
   r >>= 8;
   const bool neg = (r & 1) != 0;
   const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-  double x = __dmul_rn(double(rabs), wi[idx]);
+  double x = __dmul_rn(double(rabs), t.wi[idx]);
   if (neg) x = -x;
-  double val = x;
-  int code;
-  if (rabs < ki[idx]) {
+  val = x;
+  if (rabs < t.ki[idx]) {
     code = (1 << 30) | 1;
   } else if (idx == 0) {
     code = 0;  // runs past the generated words unless accepted below
@@ -154,14 +157,26 @@ __global__ void __launch_bounds__(256) classify_kernel(const uint64_t *Rall, int
     }
   } else if (p + 1 < L) {
     const double u = next_double(R[p + 1]);
-    const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(fi[idx - 1], -fi[idx]), u),
-                                 fi[idx]);
+    const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(t.fi[idx - 1], -t.fi[idx]), u), t.fi[idx]);
     const bool acc = lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x));
     code = (acc ? (1 << 30) : 0) | 2;
   } else {
     code = 0;
   }
-  valall[s * L + p] = val;
+}
+
+__global__ void __launch_bounds__(256) classify_kernel(const uint64_t *Rall, int64_t L,
+                                                      double *valall, int *codeall) {
+  __shared__ ZigTables t;
+  load_tables(t);
+  __syncthreads();
+  const int s = blockIdx.y;
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= L) return;
+  double val;
+  int code;
+  draw_at(Rall + s * L, L, p, t, val, code);
+  if (valall) valall[s * L + p] = val;
   codeall[s * L + p] = code;
 }
 
@@ -360,6 +375,263 @@ __global__ void emit_kernel(const double *valall, int64_t L, int64_t count, cons
   if (idx < count) out[s * ldo + idx] = valall[s * L + p];
 }
 
+// ---------------------------------------------------------------------------
+// Large draws (count > kMaxCount, one stream): the same passes with the
+// non-trivial positions in global memory and every scan split into a
+// per-block pass, a one-CTA scan of the block totals and an apply pass.
+
+constexpr int64_t kMaxLarge = int64_t(1) << 30;
+constexpr int kScanBlock = 1024;  // entries per block of the special-list scans
+
+__host__ __device__ inline int64_t large_cap(int64_t L) { return L / 32 + 8192; }
+
+struct LargeWs {
+  uint64_t *R;
+  int *code, *off;  // off[nch + 1]: exclusive chunk offsets, off[nch] = #specials
+  int *sp_pos, *sp_code, *sp_flags, *sp_dex, *sp_din, *sp_cover;
+  double *sp_val;
+  int *blk_a, *blk_b;
+  int64_t L, nch, cap, nblk;
+};
+__host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
+__host__ __device__ inline size_t large_bytes(int64_t count, LargeWs *w, uint8_t *base) {
+  const int64_t L = raw_len(count), nch = (L + kChunkPos - 1) / kChunkPos, cap = large_cap(L);
+  const int64_t nblk = (cap + kScanBlock - 1) / kScanBlock;
+  size_t o = 256;
+  auto take = [&](size_t bytes) { const size_t at = o; o = align8(o + bytes); return at; };
+  const size_t oR = take(8 * L), oc = take(4 * L), oo = take(4 * (nch + 1));
+  const size_t op = take(4 * cap), oq = take(4 * cap), of = take(4 * cap), od = take(4 * cap),
+               oi = take(4 * cap), ov = take(4 * cap), ol = take(8 * cap);
+  const size_t oa = take(4 * nblk), ob = take(4 * nblk);
+  if (w) {
+    w->R = reinterpret_cast<uint64_t *>(base + oR);
+    w->code = reinterpret_cast<int *>(base + oc);
+    w->off = reinterpret_cast<int *>(base + oo);
+    w->sp_pos = reinterpret_cast<int *>(base + op);
+    w->sp_code = reinterpret_cast<int *>(base + oq);
+    w->sp_flags = reinterpret_cast<int *>(base + of);
+    w->sp_dex = reinterpret_cast<int *>(base + od);
+    w->sp_din = reinterpret_cast<int *>(base + oi);
+    w->sp_cover = reinterpret_cast<int *>(base + ov);
+    w->sp_val = reinterpret_cast<double *>(base + ol);
+    w->blk_a = reinterpret_cast<int *>(base + oa);
+    w->blk_b = reinterpret_cast<int *>(base + ob);
+    w->L = L; w->nch = nch; w->cap = cap; w->nblk = nblk;
+  }
+  return o;
+}
+
+__device__ __forceinline__ int reach_of(int pos, int code, int64_t L) {
+  const int len = code & 0x3fffffff;
+  return len ? pos + len : int(L);
+}
+
+// special positions per 2048-position chunk (a warp per chunk)
+__global__ void chunk_count_kernel(const int *code, int64_t L, int64_t nch, int *cnt) {
+  const int64_t c = int64_t(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c >= nch) return;
+  int n = 0;
+  for (int64_t p = c * kChunkPos + lane; p < min(L, (c + 1) * kChunkPos); p += 32)
+    n += code[p] != kFast;
+  n = __reduce_add_sync(0xffffffffu, n);
+  if (lane == 0) cnt[c] = n;
+}
+
+// in-place exclusive scan (sum or max) of v[0..n) by one 1024-thread CTA;
+// v[n] receives the total when `total_slot`
+template <bool MAX>
+__global__ void __launch_bounds__(kResolveThreads, 1)
+    scan_inplace_kernel(int *v, int64_t n, bool total_slot, int64_t cap, int *status) {
+  __shared__ int warp_sums[32];
+  const int64_t per = (n + kResolveThreads - 1) / kResolveThreads;
+  const int64_t a = min(n, per * threadIdx.x), b = min(n, a + per);
+  int loc = MAX ? INT_MIN : 0;
+  for (int64_t k = a; k < b; ++k) loc = MAX ? max(loc, v[k]) : loc + v[k];
+  int ex;
+  const int tot = block_scan<MAX>(loc, warp_sums, ex);
+  for (int64_t k = a; k < b; ++k) {
+    const int x = v[k];
+    v[k] = ex;
+    ex = MAX ? max(ex, x) : ex + x;
+  }
+  if (threadIdx.x == 0 && total_slot) {
+    v[n] = tot;
+    if (!MAX && tot > cap) atomicMax(status, 2);
+  }
+}
+
+// compaction in order (ballot per 32 positions) plus each special's value
+__global__ void compact_kernel(const uint64_t *R, int64_t L, const int *code, int64_t nch,
+                               const int *off, int64_t cap, int *sp_pos, int *sp_code,
+                               double *sp_val, int *sp_flags) {
+  __shared__ ZigTables t;
+  load_tables(t);
+  __syncthreads();
+  const int64_t c = int64_t(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c >= nch || off[nch] > cap) return;
+  int o = off[c];
+  for (int64_t p0 = c * kChunkPos; p0 < min(L, (c + 1) * kChunkPos); p0 += 32) {
+    const int64_t p = p0 + lane;
+    const int cd = p < L ? code[p] : kFast;
+    const unsigned m = __ballot_sync(0xffffffffu, cd != kFast);
+    if (cd != kFast) {
+      const int k = o + __popc(m & ((1u << lane) - 1));
+      double v;
+      int c2;
+      draw_at(R, L, p, t, v, c2);
+      sp_pos[k] = int(p);
+      sp_code[k] = cd;
+      sp_val[k] = v;
+      sp_flags[k] = 0;
+    }
+    o += __popc(m);
+  }
+}
+
+// per block of 1024 entries: max reach (blk_a) -- the prefix-max scan's block totals
+__global__ void __launch_bounds__(kScanBlock) reach_block_kernel(const int *sp_pos,
+                                                                const int *sp_code,
+                                                                const int *nsp_p, int64_t L,
+                                                                int *blk) {
+  __shared__ int red[32];
+  const int nsp = *nsp_p;
+  const int64_t k = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
+  int r = k < nsp ? reach_of(sp_pos[k], sp_code[k], L) : INT_MIN;
+  r = __reduce_max_sync(0xffffffffu, r);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = red[threadIdx.x];
+    v = __reduce_max_sync(0xffffffffu, v);
+    if (threadIdx.x == 0) blk[blockIdx.x] = v;
+  }
+}
+
+// heads (no earlier entry reaches them) start clusters; the head's thread
+// walks its cluster and writes the start/emit flags of every entry in it
+__global__ void __launch_bounds__(kScanBlock) walk_kernel(const int *sp_pos, const int *sp_code,
+                                                         const int *nsp_p, int64_t L,
+                                                         const int *blkpre, int *sp_flags) {
+  __shared__ int warp_sums[32];
+  const int nsp = *nsp_p;
+  const int64_t k = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
+  const int rk = k < nsp ? reach_of(sp_pos[k], sp_code[k], L) : INT_MIN;
+  int ex;
+  block_scan<true>(rk, warp_sums, ex);
+  if (k >= nsp) return;
+  const int pm = max(ex, blkpre[blockIdx.x]);
+  if (pm > sp_pos[k]) return;  // inside some earlier range: not a head
+  int cur = rk, pmw = max(pm, rk);
+  sp_flags[k] = 1 | (((sp_code[k] >> 30) & 1) << 1);
+  for (int64_t j = k + 1; j < nsp; ++j) {
+    const int pj = sp_pos[j];
+    if (pmw <= pj) break;  // the next head
+    const int cj = sp_code[j], rj = reach_of(pj, cj, L);
+    if (pj >= cur) {
+      sp_flags[j] = 1 | (((cj >> 30) & 1) << 1);
+      cur = rj;
+    }
+    pmw = max(pmw, rj);
+  }
+}
+
+__device__ __forceinline__ int nonemit_of(int pos, int code, int flags, int64_t L) {
+  if (!(flags & 1)) return 0;
+  return (reach_of(pos, code, L) - pos - 1) + ((flags & 2) ? 0 : 1);
+}
+
+// per block: sum of the words starts consume without a value (blk_a) and the
+// max start reach (blk_b)
+__global__ void __launch_bounds__(kScanBlock) dsum_block_kernel(const int *sp_pos,
+                                                               const int *sp_code,
+                                                               const int *sp_flags,
+                                                               const int *nsp_p, int64_t L,
+                                                               int *blk_sum, int *blk_max) {
+  __shared__ int rs[32], rm[32];
+  const int nsp = *nsp_p;
+  const int64_t k = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
+  int ne = 0, cm = 0;
+  if (k < nsp) {
+    const int f = sp_flags[k];
+    ne = nonemit_of(sp_pos[k], sp_code[k], f, L);
+    cm = (f & 1) ? reach_of(sp_pos[k], sp_code[k], L) : 0;
+  }
+  ne = __reduce_add_sync(0xffffffffu, ne);
+  cm = __reduce_max_sync(0xffffffffu, cm);
+  if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = ne; rm[threadIdx.x >> 5] = cm; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int a = __reduce_add_sync(0xffffffffu, rs[threadIdx.x]);
+    int m = __reduce_max_sync(0xffffffffu, rm[threadIdx.x]);
+    if (threadIdx.x == 0) { blk_sum[blockIdx.x] = a; blk_max[blockIdx.x] = m; }
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) dapply_kernel(
+    const int *sp_pos, const int *sp_code, const int *sp_flags, const int *nsp_p, int64_t L,
+    int64_t count, const int *blk_sum, const int *blk_max, int *sp_dex, int *sp_din,
+    int *sp_cover, int *status) {
+  __shared__ int warp_sums[32];
+  const int nsp = *nsp_p;
+  const int64_t k = int64_t(blockIdx.x) * kScanBlock + threadIdx.x;
+  int ne = 0, cr = 0, f = 0;
+  if (k < nsp) {
+    f = sp_flags[k];
+    ne = nonemit_of(sp_pos[k], sp_code[k], f, L);
+    cr = (f & 1) ? reach_of(sp_pos[k], sp_code[k], L) : 0;
+  }
+  int dex, cex;
+  block_scan<false>(ne, warp_sums, dex);
+  block_scan<true>(cr, warp_sums, cex);
+  if (k >= nsp) return;
+  dex += blk_sum[blockIdx.x];
+  const int cover = max(max(cex, blk_max[blockIdx.x]), cr);
+  sp_dex[k] = dex;
+  sp_din[k] = dex + ne;
+  sp_cover[k] = max(cover, 0);
+  if ((f & 1) && (sp_code[k] & 0x3fffffff) == 0 && sp_pos[k] - dex < count)
+    atomicMax(status, 1);  // a needed draw runs past the generated words
+  if (k == nsp - 1 && L - (dex + ne) < count) atomicMax(status, 1);
+}
+
+__global__ void emit_large_kernel(const uint64_t *R, int64_t L, int64_t count, const int *off,
+                                  int64_t nch, const int *sp_pos, const int *sp_flags,
+                                  const int *sp_dex, const int *sp_din, const int *sp_cover,
+                                  const double *sp_val, int64_t cap, double *out) {
+  __shared__ double wi[256];
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) wi[e] = zig::wi[e];
+  __syncthreads();
+  const int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= L || off[nch] > cap) return;
+  const int64_t c = p / kChunkPos;
+  int lo = off[c], hi = off[c + 1];
+  const int first = lo;
+  while (lo < hi) {  // first entry of this chunk with pos > p
+    const int mid = (lo + hi) >> 1;
+    if (sp_pos[mid] <= p) lo = mid + 1; else hi = mid;
+  }
+  const int k = lo - 1;  // last entry with pos <= p (the previous chunk's last if lo == first)
+  (void)first;
+  int64_t idx;
+  double v;
+  if (k >= 0 && sp_pos[k] == p) {
+    if (sp_flags[k] != 3) return;
+    idx = p - sp_dex[k];
+    v = sp_val[k];
+  } else {
+    if (k >= 0 && sp_cover[k] > p) return;
+    idx = p - (k >= 0 ? sp_din[k] : 0);
+    uint64_t r = R[p];  // a one-word draw: recompute its value
+    const int layer = int(r & 0xff);
+    r >>= 8;
+    v = __dmul_rn(double((r >> 1) & 0x000fffffffffffffull), wi[layer]);
+    if (r & 1) v = -v;
+  }
+  if (idx < count) out[idx] = v;
+}
+
 }  // namespace rng
 }  // namespace sap
 
@@ -368,18 +640,64 @@ using namespace sap;
 extern "C" {
 
 size_t sap_normal_workspace(int64_t count, int nstreams) {
+  if (count > rng::kMaxCount) return rng::large_bytes(count, nullptr, nullptr);
   const int64_t L = rng::raw_len(count);
   return 256 + size_t(nstreams) * size_t(L) * (8 + 8 + 4) +
          size_t(nstreams) * (5 * rng::kMaxSpecial + 32) * sizeof(int);
 }
 
+// one stream of more than kMaxCount normals (rng.cu "Large draws")
+static int normal_fill_large(const uint64_t *states, int64_t count, double *out, void *ws,
+                             cudaStream_t st) {
+  using namespace rng;
+  LargeWs w;
+  large_bytes(count, &w, static_cast<uint8_t *>(ws));
+  int *status = static_cast<int *>(ws);
+  int rc;
+  if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
+    return fail(SAP_ERR_DEVICE, "normal_fill: memset failed");
+  const int64_t L = w.L;
+  {
+    const int64_t threads = (L + kChunk - 1) / kChunk;
+    raw_kernel<<<dim3(unsigned((threads + 255) / 256), 1), 256, 0, st>>>(states, L, w.R);
+    if ((rc = check_launch("normal_raw_kernel")) != SAP_OK) return rc;
+  }
+  classify_kernel<<<dim3(unsigned((L + 255) / 256), 1), 256, 0, st>>>(w.R, L, nullptr, w.code);
+  if ((rc = check_launch("normal_classify_kernel")) != SAP_OK) return rc;
+  const unsigned cgrid = unsigned((w.nch + 7) / 8);
+  chunk_count_kernel<<<cgrid, 256, 0, st>>>(w.code, L, w.nch, w.off);
+  scan_inplace_kernel<false><<<1, kResolveThreads, 0, st>>>(w.off, w.nch, true, w.cap, status);
+  compact_kernel<<<cgrid, 256, 0, st>>>(w.R, L, w.code, w.nch, w.off, w.cap, w.sp_pos, w.sp_code,
+                                        w.sp_val, w.sp_flags);
+  const int *nsp = w.off + w.nch;
+  const unsigned bgrid = unsigned(w.nblk);
+  reach_block_kernel<<<bgrid, kScanBlock, 0, st>>>(w.sp_pos, w.sp_code, nsp, L, w.blk_a);
+  scan_inplace_kernel<true><<<1, kResolveThreads, 0, st>>>(w.blk_a, w.nblk, false, 0, status);
+  walk_kernel<<<bgrid, kScanBlock, 0, st>>>(w.sp_pos, w.sp_code, nsp, L, w.blk_a, w.sp_flags);
+  dsum_block_kernel<<<bgrid, kScanBlock, 0, st>>>(w.sp_pos, w.sp_code, w.sp_flags, nsp, L, w.blk_a,
+                                                  w.blk_b);
+  scan_inplace_kernel<false><<<1, kResolveThreads, 0, st>>>(w.blk_a, w.nblk, false, 0, status);
+  scan_inplace_kernel<true><<<1, kResolveThreads, 0, st>>>(w.blk_b, w.nblk, false, 0, status);
+  dapply_kernel<<<bgrid, kScanBlock, 0, st>>>(w.sp_pos, w.sp_code, w.sp_flags, nsp, L, count,
+                                              w.blk_a, w.blk_b, w.sp_dex, w.sp_din, w.sp_cover,
+                                              status);
+  emit_large_kernel<<<unsigned((L + 255) / 256), 256, 0, st>>>(
+      w.R, L, count, w.off, w.nch, w.sp_pos, w.sp_flags, w.sp_dex, w.sp_din, w.sp_cover,
+      w.sp_val, w.cap, out);
+  return check_launch("normal_emit_large_kernel");
+}
+
 int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double *out, int64_t ldo,
                     void *ws, size_t ws_bytes, void *stream) {
-  if (nstreams <= 0 || count <= 0 || count > rng::kMaxCount || ldo < count)
-    return fail(SAP_ERR_CONTRACT, "normal_fill: bad shape streams=%d count=%lld ldo=%lld",
+  if (nstreams <= 0 || count <= 0 || count > rng::kMaxLarge || ldo < count ||
+      (count > rng::kMaxCount && nstreams != 1))
+    return fail(SAP_ERR_CONTRACT, "normal_fill: bad shape streams=%d count=%lld ldo=%lld "
+                "(more than 2^20 normals: one stream at a time, at most 2^30)",
                 nstreams, (long long)count, (long long)ldo);
   if (!ws || ws_bytes < sap_normal_workspace(count, nstreams))
     return fail(SAP_ERR_CONTRACT, "normal_fill: workspace too small");
+  if (count > rng::kMaxCount)
+    return normal_fill_large(states, count, out, ws, reinterpret_cast<cudaStream_t>(stream));
   const int64_t L = rng::raw_len(count);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t *w = static_cast<uint8_t *>(ws);

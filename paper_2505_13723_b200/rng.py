@@ -83,3 +83,22 @@ class DeviceNormals:
     def status(self):
         """Device int32 status of the last fill (0 = ok); reading it syncs."""
         return self.ws.view(dtype=__import__("torch").int32)[0]
+
+
+def standard_normal(gen, shape, device=None):
+    """``gen.standard_normal(shape)`` -- the same numbers, drawn on the GPU
+    (csrc/rng.cu) when ``device`` is a CUDA device and the draw is large
+    (>= 2^16 values, at most 2^30); returns a float64 torch tensor on the
+    device then, a numpy array otherwise. ``gen`` must be fresh (nothing drawn
+    from it yet); it is left untouched by the device path."""
+    import math
+    import torch
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    count = math.prod(shape)
+    dev = torch.device(device) if device is not None else None
+    if dev is None or dev.type != "cuda" or not (1 << 16) <= count <= (1 << 30):
+        return gen.standard_normal(shape)
+    states = torch.tensor([pcg64_words(gen)], dtype=torch.int64, device=dev)
+    out = torch.empty((1, count), dtype=torch.float64, device=dev)
+    DeviceNormals(count, 1, dev).fill(states, out)
+    return out.view(shape)

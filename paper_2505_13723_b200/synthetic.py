@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .rng import substream
+from .rng import standard_normal, substream
 
 
 @dataclass
@@ -132,7 +132,8 @@ def make_problem(n, d, family="rbf", m=9, seed=0, lam=1e-2, q=2048,
     yall = (yall - ymu) / ysd
     y = yall[:n]
     if rhs == "pathwise":
-        zeta = math.sqrt(lam) * substream(seed, "zeta").standard_normal((n, s))
+        z = standard_normal(substream(seed, "zeta"), (n, s), device)
+        zeta = math.sqrt(lam) * (z.cpu().numpy() if torch.is_tensor(z) else z)
         Y = np.concatenate([y[:, None], y[:, None] - vals[:n, 1:] - zeta], axis=1)
         f_test = vals[n:, 1:]
     else:

@@ -63,8 +63,8 @@ t0 = time.perf_counter()
 prob = synthetic.make_problem(n, d, a.family, m, seed=0, lam=1e-2, device=dev)
 res["prior_rhs"] = {"make_problem_seconds_host_timed": time.perf_counter() - t0,
                     "what": "make_problem: phi(X) theta for n + 10^4 points, q=2048 cosine "
-                            "features, 65 columns (fused tensor-core product), plus the host "
-                            "numpy draws (X, noise, zeta: n x 64 normals)"}
+                            "features, 65 columns (fused tensor-core product), zeta (n x 64) drawn "
+                            "on the GPU, host numpy X and noise; first CUDA use in the process"}
 from paper_2505_13723_b200.kernels import cos_features_times  # noqa: E402
 from paper_2505_13723_b200.synthetic import feature_map  # noqa: E402
 from paper_2505_13723_b200.rng import substream  # noqa: E402

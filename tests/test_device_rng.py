@@ -108,3 +108,23 @@ def test_device_normals_many_streams_statistics():
     got = out.cpu().numpy()
     mism = sum(assert_numpy_equal(got[i], gens[i].standard_normal(count), i) for i in range(ns))
     assert mism <= 64  # 1-ulp tail values: 8 measured in 12.8M draws
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("count", [(1 << 20) + 1, 5_000_000, 21_000_000])
+def test_device_normals_large_counts(count):
+    """One stream of more than 2^20 normals (the multi-CTA passes): e.g. the
+    pathwise-sampling noise zeta = substream(seed, "zeta").standard_normal((n, s))
+    (gp.py:221) or PCG's (n, r) test matrix (solvers.py:538)."""
+    import torch
+    from paper_2505_13723_b200.rng import DeviceNormals
+    dev = torch.device("cuda", 0)
+    g = substream(0, "zeta")
+    states = torch.tensor([pcg64_words(g)], dtype=torch.int64, device=dev)
+    dn = DeviceNormals(count, 1, dev)
+    out = torch.empty((1, count), dtype=torch.float64, device=dev)
+    dn.fill(states, out)
+    assert int(dn.status()) == 0
+    got = out[0].cpu().numpy()
+    mism = assert_numpy_equal(got, g.standard_normal(count), count)
+    assert mism <= max(8, count // 200_000)
