@@ -100,6 +100,10 @@ def init_from_env(backend=None):
     if backend is None:
         backend = "nccl" if torch.cuda.is_available() else "gloo"
     if backend == "nccl":
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-    tdist.init_process_group(backend=backend)
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        # bind the communicator to this rank's GPU up front (no device guessing)
+        tdist.init_process_group(backend=backend, device_id=torch.device("cuda", local))
+    else:
+        tdist.init_process_group(backend=backend)
     return True
