@@ -19,7 +19,7 @@
  *                          KernelOracle.tile + family values    kernels.py:56-66, :118-127
  *                          KernelOracle.cross_matmul            kernels.py:161-176
  *                          KernelOracle.matmul                  kernels.py:145-159
- *   sap_ktile           <- KernelOracle.tile / .block / .dense   kernels.py:118-143
+ *   sap_ktile(64)       <- KernelOracle.tile / .block / .dense   kernels.py:118-143
  *   sap_grad_gather     <- grad = K[B,:]Z + lam Z[B] - Y[B]     solvers.py:376-377
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_combine         <- materialising W (or Z) from the lazy
@@ -104,6 +104,15 @@ int sap_ktile(const float *Ra, const float *rasqn, const int64_t *row_ids, int64
               const float *Rc, const float *rcsqn, const int64_t *col_ids, int64_t nc,
               int ldx, int d, int family, double variance, double *out, int64_t ldo,
               void *stream);
+
+/*
+ * Dense K[row_ids, col_ids] in the reference's fp64 arithmetic from the fp64
+ * points X (n x d row-major) and 1/lengthscale (d): the dense-access API
+ * (KernelOracle.tile/block/dense, kernels.py:118-143); bitwise symmetric.
+ */
+int sap_ktile64(const double *X, const double *inv_ls, int d, const int64_t *row_ids, int64_t na,
+                const int64_t *col_ids, int64_t nc, int family, double variance, double *out,
+                int64_t ldo, void *stream);
 
 /* sap_ktile with fp32 output (the same fp32-computed values, half the bytes). */
 int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, int64_t na,

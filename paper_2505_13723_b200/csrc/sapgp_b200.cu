@@ -113,6 +113,48 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
+// fp64 tile for the dense-access API (KernelOracle.tile/block/dense,
+// kernels.py:118-143): the reference's own arithmetic -- z = x / l in fp64,
+// sq = |z_r|^2 + |z_c|^2 - 2 z_r.z_c, sq = 0 where the ids match, clamp at 0,
+// family values in fp64 -- so dense blocks are PSD to fp64 rounding (the
+// hot path's K_BB uses the fp32 tile above).
+template <int FAM>
+__device__ __forceinline__ double kernel_value64(double sq) {
+  sq = fmax(sq, 0.0);
+  if constexpr (FAM == SAP_RBF) {
+    return exp(-0.5 * sq);
+  } else if constexpr (FAM == SAP_MATERN32) {
+    const double a = 1.7320508075688772 * sqrt(sq);
+    return (1.0 + a) * exp(-a);
+  } else {
+    const double a = 2.23606797749979 * sqrt(sq);
+    return (1.0 + a + (5.0 / 3.0) * sq) * exp(-a);
+  }
+}
+
+template <int FAM>
+__global__ void ktile64_kernel(const double *X, const double *inv_ls, int d,
+                               const int64_t *row_ids, int64_t na, const int64_t *col_ids,
+                               int64_t nc, double variance, double *out, int64_t ldo) {
+  const int64_t i = int64_t(blockIdx.y) * blockDim.y + threadIdx.y;
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= na || j >= nc) return;
+  const int64_t ri = row_ids[i], cj = col_ids[j];
+  double v = variance;
+  if (ri != cj) {
+    double nr = 0.0, ncs = 0.0, dot = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double zr = X[ri * d + k] * inv_ls[k], zc = X[cj * d + k] * inv_ls[k];
+      nr = fma(zr, zr, nr);
+      ncs = fma(zc, zc, ncs);
+      dot = fma(zr, zc, dot);
+    }
+    v = variance * kernel_value64<FAM>(nr + ncs - 2.0 * dot);
+  }
+  out[i * ldo + j] = v;
+}
+
 // ---------------------------------------------------------------------------
 // gradient gather (solvers.py:376-377), lazy Nesterov rows, materialisation
 
@@ -503,6 +545,31 @@ int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int 
   sdd_dense_kernel<<<unsigned((rows4 + 255) / 256), 256, 0, S(stream)>>>(
       V, W, E, ldv, rows4, m, VB, pos, float(momentum), float(avg));
   return check_launch("sdd_dense_kernel");
+}
+
+int sap_ktile64(const double *X, const double *inv_ls, int d, const int64_t *row_ids, int64_t na,
+                const int64_t *col_ids, int64_t nc, int family, double variance, double *out,
+                int64_t ldo, void *stream) {
+  if (na <= 0 || nc <= 0 || d < 1 || ldo < nc)
+    return fail(SAP_ERR_CONTRACT, "ktile64: bad shape");
+  dim3 blk(32, 8), grid(unsigned((nc + 31) / 32), unsigned((na + 7) / 8));
+  cudaStream_t st = S(stream);
+  switch (family) {
+    case SAP_RBF:
+      ktile64_kernel<SAP_RBF><<<grid, blk, 0, st>>>(X, inv_ls, d, row_ids, na, col_ids, nc,
+                                                    variance, out, ldo);
+      break;
+    case SAP_MATERN32:
+      ktile64_kernel<SAP_MATERN32><<<grid, blk, 0, st>>>(X, inv_ls, d, row_ids, na, col_ids, nc,
+                                                         variance, out, ldo);
+      break;
+    case SAP_MATERN52:
+      ktile64_kernel<SAP_MATERN52><<<grid, blk, 0, st>>>(X, inv_ls, d, row_ids, na, col_ids, nc,
+                                                         variance, out, ldo);
+      break;
+    default: return fail(SAP_ERR_CONTRACT, "ktile64: unknown family %d", family);
+  }
+  return check_launch("ktile64_kernel");
 }
 
 }  // extern "C"

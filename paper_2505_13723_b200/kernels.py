@@ -374,13 +374,20 @@ class KernelOracle:
             return np.zeros((r.numel(), c.numel()))
         if int(r.min()) < 0 or int(r.max()) >= self.n or int(c.min()) < 0 or int(c.max()) >= self.n:
             raise ContractError("tile index out of range")
-        A, asq = self.points.gather(r)
-        C, csq = self.points.gather(c)
-        return ktile(self.spec, A, asq, r, C, csq, c, self.points.ldx, self.d).cpu().numpy()
+        return self._tile64(r, c).cpu().numpy()
+
+    def _tile64(self, r, c):
+        """fp64 K[r, c] in the reference's arithmetic (sap_ktile64)."""
+        out = torch.empty((r.numel(), c.numel()), dtype=torch.float64, device=self.device)
+        inv = torch.as_tensor(np.broadcast_to(1.0 / self.spec.lengthscales, (self.d,)).copy(),
+                              device=self.device)
+        nat.call("sap_ktile64", nat.ptr(self._Xd), nat.ptr(inv), self.d, nat.ptr(r), r.numel(),
+                 nat.ptr(c), c.numel(), self.spec.code, self.spec.variance, nat.ptr(out),
+                 out.stride(0), nat.stream_handle())
+        return out
 
     def block_device(self, block_dev):
-        A, asq = self.points.gather(block_dev)
-        return ktile(self.spec, A, asq, block_dev, A, asq, block_dev, self.points.ldx, self.d)
+        return self._tile64(block_dev, block_dev)
 
     def block(self, block):
         """Exact symmetric K[block, block] with the variance on the diagonal."""
