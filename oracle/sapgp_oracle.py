@@ -418,6 +418,26 @@ def _due(every, t, total):
     return (t + 1) % every == 0 or t == total - 1
 
 
+def sap_solve(pts, lam, Y, iters, seed, b, residual_every=0, workers=1):
+    """solvers.py:269-348 (uniform sampler, no tail averaging) -- exact projection
+    steps: (K[B,B] + lam I) d = K[B,:] W + lam W[B] - Y[B] by one Cholesky,
+    W[B] -= d. Returns (W, residual trace, crc32 per block)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    Y2 = Y[:, None] if Y.ndim == 1 else Y
+    W = np.zeros_like(Y2)
+    res, crcs = [], []
+    for t in range(iters):
+        block = uniform_block(seed, t, pts.n, b)
+        grad = col_dist_matmul(pts, W, block, workers) + lam * W[block] - Y2[block]
+        H = block_block(pts, block)
+        H[np.diag_indices_from(H)] += lam
+        W[block] -= scipy.linalg.cho_solve(scipy.linalg.cho_factor(H, lower=True), grad)
+        res.append(relative_residual(pts, lam, W, Y2) if _due(residual_every, t, iters)
+                   else math.nan)
+        crcs.append(block_crc(block))
+    return (W[:, 0] if Y.ndim == 1 else W), np.array(res), np.array(crcs, dtype=np.int64)
+
+
 def sdd_solve(pts, lam, Y, iters, seed, b, scale=10.0, residual_every=0, workers=1):
     """solvers.py:463-516 -- block stochastic dual descent: raw block gradient,
     stepsize scale/n, heavy-ball momentum 0.9, geometric averaging 100/T.

@@ -95,7 +95,7 @@ def _relres_cm(oracle, shard, Xcm, Ycm, lam, ynorm):
         part = torch.zeros(1, dtype=torch.float64, device=oracle.device)
     else:
         ids = torch.arange(shard.lo, shard.hi, device=oracle.device, dtype=torch.int64)
-        KX = oracle.rows_times_device(ids, Xfull)
+        KX = oracle.rows_times_device(ids, Xfull.to(torch.float32).contiguous())
         res = KX.double() + lam * Xloc.double() - Ycm[:, :nl].T.double()
         part = (res * res).sum().reshape(1)
     allreduce_sum_(part)
@@ -309,3 +309,101 @@ def pcg_solve(oracle, Y, config, pool=None, on_iterate=None):
         trace.record(done, float(done), float(torch.linalg.vector_norm(R)) / ynorm, math.nan, 0)
     Xh = X.cpu().numpy()
     return SolveResult(Xh[:, 0] if vector else Xh, trace, False, done, float(done))
+
+
+class SapEngine(SddEngine):
+    """Exact sketch-and-project (solvers.py:269-287): the block gradient on the
+    same block product, then (K[B,B] + lam I) d = grad by one fp64 Cholesky of
+    size b on the device (cuSOLVER through torch.linalg), W[B] -= d. K[B,B] is
+    the fp64 tile (sap_ktile64, the reference's arithmetic)."""
+
+    def __init__(self, oracle, Y, config, total, shard=None):
+        super().__init__(oracle, Y, config, total, shard)
+        if self.shard.world > 1:
+            raise ConfigError("exact SAP runs on one device (its b x b solve is not sharded)")
+        self.info = torch.zeros((), dtype=torch.int32, device=self.dev)
+        # the iterate in fp64 (the exact projection is an fp64 solve, state.W of
+        # the reference); self.W is its fp32 copy, the block product's operand
+        self.W64 = torch.zeros((self.m, self.ld), dtype=torch.float64, device=self.dev)
+        Ya = np.asarray(Y, dtype=np.float64)
+        Yl = Ya[self.shard.lo:self.shard.hi]
+        Yl = Yl[:, None] if Yl.ndim == 1 else Yl
+        self.Y64 = torch.zeros((self.m, self.ld), dtype=torch.float64, device=self.dev)
+        self.Y64[:, :Yl.shape[0]] = torch.as_tensor(Yl.T, device=self.dev)
+
+    def step(self):
+        blk, crc, bd = self.feed.get()
+        b, m = self.b, self.m
+        loc = self.shard.local_positions(bd)
+        if self.use_tc:
+            self.zop.fill(self.W)
+            self.tcp.gather_rows(bd, out=self.RAg)
+            krows_tc(self.o.spec, self.tcp, self.RAg, b, bd, self.zop, self.G, ws=self.ws)
+        else:
+            pts = self.o.points
+            Xb, rsq = pts.gather(bd)
+            krows_times(self.o.spec, pts, Xb, rsq, bd, self.W, self.G, col_base=self.shard.lo,
+                        ws=self.ws, ncols=self.shard.size, col_offset=self.shard.lo)
+        # grad = K[B,:] W + lam W[B] - Y[B], the last two terms from the fp64 iterate
+        self.g.copy_(self.G)
+        self.g += self.lam * self.W64[:, loc].T - self.Y64[:, loc].T
+        H = self.o.block_device(bd)
+        H.diagonal().add_(self.lam)
+        L, info = torch.linalg.cholesky_ex(H)
+        self.info = torch.maximum(self.info, info)  # checked at the end of the solve
+        d = torch.cholesky_solve(self.g, L)
+        self.W64[:, loc] -= d.T
+        self.W[:, loc] = self.W64[:, loc].float()
+        self.t += 1
+        return blk, crc
+
+    def iterate_local(self):
+        return self.W64[:, :self.shard.size].T
+
+
+def sap_solve(oracle, Y, config, sampler="uniform", dpp_model=None, pool=None, on_iterate=None):
+    """Exact sketch-and-project from W0 = 0 with optional tail averaging
+    (solvers.py:290-348). The k-DPP sampler (dpp.py) is outside the B200 build.
+    A failed block Cholesky raises NumericalError at the end of the solve (the
+    device flags are read once, not per step)."""
+    from .solvers import (ConvergenceTrace, SolveResult, TailAverager, _due, _to_host64,
+                          _y_norm, budget_iterations, resolve_blocksize)
+    if sampler != "uniform":
+        if sampler == "kdpp":
+            raise ConfigError("k-DPP block sampling is outside the B200 build")
+        raise ConfigError(f"unknown sampler {sampler!r}")
+    n = oracle.n
+    b = resolve_blocksize(config, n)
+    total = budget_iterations(config, b / n)
+    eng = SapEngine(oracle, Y, config, total)
+    try:
+        ynorm = _y_norm(Y)
+        trace = ConvergenceTrace()
+        averager = TailAverager(total, (n, eng.m)) if config.tail_average else None
+        diverged, done = False, 0
+        for t in range(total):
+            blk, crc = eng.step()
+            done = t + 1
+            if averager is not None:
+                averager.add(done, eng.iterate_local().clone())
+            if on_iterate is not None:
+                on_iterate(done, _to_host64(eng.iterate_local()))
+            relres = math.nan
+            if _due(config.residual_every, t, total):
+                relres = _relres_cm(oracle, eng.shard, eng.W64, eng.Y64, eng.lam, ynorm)
+            trace.record(done, done * b / n, relres, 1.0, crc)
+            if np.isfinite(relres):
+                if relres > DIVERGENCE_FACTOR or not bool(torch.isfinite(eng.W64).all()):
+                    diverged = True
+                    break
+                if config.tol is not None and relres <= config.tol:
+                    break
+        if int(eng.info) != 0:
+            raise NumericalError("block system factorization failed; lam may be too small "
+                                 "for float64")
+        W_loc = averager.average() if averager is not None and averager.count > 0 else \
+            eng.iterate_local()
+        W = _to_host64(W_loc)
+    finally:
+        eng.close()
+    return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)

@@ -579,8 +579,8 @@ def solve(oracle, Y, config, dpp_model=None, pool=None, on_iterate=None):
     """Dispatch on ``config.solver_id`` (solvers.py:591-615).
 
     The B200 build implements the ADASAP hot path (``adasap``, ``adasap_i``)
-    and the SDD and Nystrom-PCG baselines on the same kernel (baselines.py);
-    exact SAP (a dense b x b Cholesky per iteration) is outside its scope."""
+    and the exact-SAP, SDD and Nystrom-PCG baselines on the same kernel
+    (baselines.py)."""
     if config.solver_id == "adasap":
         return adasap_solve(oracle, Y, config, on_iterate=on_iterate)
     if config.solver_id == "adasap_i":
@@ -592,5 +592,7 @@ def solve(oracle, Y, config, dpp_model=None, pool=None, on_iterate=None):
         from .baselines import pcg_solve
         return pcg_solve(oracle, Y, config, pool=pool, on_iterate=on_iterate)
     if config.solver_id == "sap":
-        raise ConfigError(f"solver {config.solver_id!r} is outside the B200 hot-path build")
+        from .baselines import sap_solve
+        return sap_solve(oracle, Y, config, sampler=config.sampler, dpp_model=dpp_model,
+                         pool=pool, on_iterate=on_iterate)
     raise ConfigError(f"unknown solver {config.solver_id!r}")

@@ -18,7 +18,7 @@ Fixtures (all float64, reference arithmetic):
                      inputs are regenerated from seeds by the tests
   randnla.npz        Nystrom factor, Woodbury applies, power stepsize
   rng.npz            block crc32s / first draws for several (seed, t, n, b)
-  baselines.npz      the SDD and Nystrom-PCG baselines (solvers.py:463-584) on
+  baselines.npz      the exact-SAP, SDD and Nystrom-PCG solvers (solvers.py:269-584) on
                      the config 1 problem: final estimates, residual traces,
                      block crc32s
 """
@@ -157,6 +157,12 @@ def baselines():
     out["sdd_res"] = np.array([r.residual for r in res.trace.records])
     out["sdd_crc"] = np.array([r.block_hash for r in res.trace.records], dtype=np.int64)
     out["sdd_eta"] = np.array([r.stepsize for r in res.trace.records])
+    cfg = sapgp.RunConfig(lam=lam, blocksize=b, solver_id="sap", max_iters=60,
+                          residual_every=10, seed=seed)
+    res = rsol.solve(orc, prob.Y, cfg)
+    out["sap_W"] = res.W
+    out["sap_res"] = np.array([r.residual for r in res.trace.records])
+    out["sap_crc"] = np.array([r.block_hash for r in res.trace.records], dtype=np.int64)
     for tag, rank in (("pcg", 100), ("cg", 0)):
         cfg = sapgp.RunConfig(lam=lam, solver_id="pcg", nystrom_rank=rank, max_iters=40,
                               seed=seed, tol=1e-6)

@@ -7,11 +7,8 @@ seeds and bars unless noted):
   #6 randomized powering         test_acceptance.py:196-219
   #7 pathwise conditioning       test_acceptance.py:222-254
 
-Deviations, each stated where it applies: exact SAP (`sap_solve`, a dense
-b x b Cholesky per step) is outside this build, so #4's full-block SAP check
-is dropped and #7 conditions with Nystrom-PCG to 1e-10 instead; block products
-are fp32-accurate (the reference is fp64), so #4's PCG-versus-dense bar is
-1e-5 instead of 1e-6.
+Deviation: block products are fp32-accurate (the reference is fp64), so #4's
+PCG-versus-dense bar is 1e-5 instead of 1e-6.
 """
 import numpy as np
 import pytest
@@ -27,8 +24,13 @@ def _dense_solve(o, lam, y):
 
 def test_criterion_04_solvers_reach_tolerance():
     rng = np.random.default_rng(6)
-    rng.uniform(-1, 1, size=(200, 2))          # the full-block SAP problem's draws
-    rng.standard_normal(200)
+    # full-block exact step equals the direct solve
+    Xs = rng.uniform(-1, 1, size=(200, 2))
+    os_ = sap.KernelOracle(sap.KernelSpec("rbf", np.array([0.5, 0.5]), 1.0), Xs, 0.3)
+    ys = rng.standard_normal(200)
+    direct = _dense_solve(os_, 0.3, ys)
+    full = sap.solve(os_, ys, sap.RunConfig(lam=0.3, solver_id="sap", blocksize=200, max_iters=1))
+    assert np.linalg.norm(full.W - direct) / np.linalg.norm(direct) <= 1e-8
     n, lam = 500, 8.0
     X = rng.uniform(-1, 1, size=(n, 2))
     o = sap.KernelOracle(sap.KernelSpec("rbf", np.array([0.15, 0.15]), 1.0), X, lam)
@@ -105,7 +107,7 @@ def test_criterion_07_pathwise_conditioning():
     cross = sap.cross_kernel(spec, Xstar, X)
     exact_mean = cross @ np.linalg.solve(A, y)
     exact_cov = sap.cross_kernel(spec, Xstar, Xstar) - cross @ np.linalg.solve(A, cross.T)
-    cfg = sap.RunConfig(lam=lam, solver_id="pcg", nystrom_rank=0, tol=1e-10, max_iters=200)
+    cfg = sap.RunConfig(lam=lam, solver_id="sap", blocksize=n, max_iters=1, residual_every=0)
 
     def solve_fn(orc, rhs):
         return sap.solve(orc, rhs, cfg).W

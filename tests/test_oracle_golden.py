@@ -107,8 +107,8 @@ def test_config1_full_solve():
 
 
 def test_oracle_baselines_match_reference():
-    """SDD and (P)CG restatements against the reference's own runs
-    (tests/golden/baselines.npz, solvers.py:463-584)."""
+    """Exact SAP, SDD and (P)CG restatements against the reference's own runs
+    (tests/golden/baselines.npz, solvers.py:269-584)."""
     g = np.load(os.path.join(GOLDEN, "baselines.npz"))
     c1 = np.load(os.path.join(GOLDEN, "config1.npz"))
     pts = orc.Points("rbf", c1["ls"], 1.0, c1["X"])
@@ -117,6 +117,10 @@ def test_oracle_baselines_match_reference():
     assert np.array_equal(crcs, g["sdd_crc"])
     np.testing.assert_allclose(est, g["sdd_W"], rtol=0, atol=1e-9 * np.abs(g["sdd_W"]).max())
     np.testing.assert_allclose(res, g["sdd_res"], rtol=1e-9)
+    W, res, crcs = orc.sap_solve(pts, 1e-2, c1["Y"], 60, 0, 200, residual_every=10, workers=4)
+    assert np.array_equal(crcs, g["sap_crc"])
+    np.testing.assert_allclose(W, g["sap_W"], rtol=0, atol=1e-9 * np.abs(g["sap_W"]).max())
+    np.testing.assert_allclose(res, g["sap_res"], rtol=1e-8)
     for tag, rank in (("pcg", 100), ("cg", 0)):
         X, res, it = orc.pcg_solve(pts, 1e-2, c1["Y"], 40, 0, rank)
         assert it == int(g[f"{tag}_iters"])
