@@ -11,15 +11,16 @@ block-row product and the update depends only on (seed, t) and X:
     eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
                                    10, substream(seed, "power", t)) :389-396
 
-so they are produced in batches by ``depth`` (default 3) host producer
-threads, up to ``depth`` batches ahead of the block-row products that consume them; their GPU work is
-enqueued in order on the solver's stream (see Lookahead.__init__).
-Batch sizes ramp 1, 2, 4, ... up to ``L = config.lookahead`` so the first
-iteration waits for one plan only, not for a full batch. Per batch there is one device->host
-round trip (three r x r matrices per iteration) for the host LAPACK part
-(``randnla.factor_core_retry``); everything dimension-b runs on the GPU in
-fp64 (QR of the sketch, U = Qs Ur, the batched power iteration). Buffers
-live in three preallocated slots reused under CUDA events, so nothing is
+so they are produced in batches by ``depth`` (default 4) host producer
+threads, up to ``depth`` batches ahead of the block-row products that
+consume them; their GPU work is enqueued in order on the solver's stream
+(see Lookahead.__init__). Batch sizes ramp 1, 2, 4, ... up to
+``L = config.lookahead`` so the first iteration waits for one plan only, not
+for a full batch. Per batch there is one device->host round trip (three
+r x r Gram matrices per iteration) for the host LAPACK part
+(``randnla.factor_gram_retry``); everything dimension-b runs on the GPU
+(Omega, the sketch, U = Y W, K[B,B], the batched power iteration). Buffers
+live in depth + 1 preallocated slots reused under CUDA events, so nothing is
 allocated in steady state.
 """
 

@@ -5,8 +5,9 @@ Same public names and semantics (``AccelParams``, ``resolve_accel``,
 ``adasap_step``, ``adasap_solve``, ``solve``), with the iteration executed
 by ``AdasapEngine``:
 
-* Phase I  -- K[B,:] Z by ``sap_krows_times`` over this rank's shard, then
-  the gradient gather g = K[B,:]Z + lam Z[B] - Y[B] (``sap_grad_gather``) and,
+* Phase I  -- K[B,:] Z over this rank's shard on the tensor-core kernel
+  (``sap_krows_tc``; ``sap_krows_times`` for shapes outside it), then the
+  gradient gather g = K[B,:]Z + lam Z[B] - Y[B] (``sap_grad_gather``) and,
   with several GPUs, one float64 all-reduce of g (paper Alg. 6);
 * Phases II/III -- produced ahead, batched, by ``pipeline.Lookahead``;
 * Phase IV -- D_B = (g - U Mc U^T g) / rho with the r x r Cholesky-stabilised
@@ -18,9 +19,9 @@ the block the recurrence (solvers.py:76-85) is the fixed linear map
 T = [[beta, 1-beta], [alpha, 1-alpha]] on the row pair (V, Z), so the
 engine stores two arrays (P, Q) and a 2 x 2 basis M with
 [V; Z] = M [P; Q] row-wise: untouched rows follow M <- T M for free, and
-the b block rows get an axpy (``sap_pq_update``). M starts at T's
-eigenbasis, which keeps it well conditioned; one column decays like
-(beta - alpha)^t and is renormalised by a rare dense rescale. W is
+the b block rows get an axpy (``sap_pq_update``). M is T's eigenbasis with
+the decaying column scaled by a scalar recurrence s_t = (beta - alpha)^t,
+renormalised by a rare dense rescale of Q. W is
 materialised only when asked for (end of solve, residuals, tail averaging,
 callbacks). DESIGN.md §4 has the derivation.
 
