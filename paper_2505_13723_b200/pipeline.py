@@ -53,11 +53,12 @@ class IterPlan:
     rsq: torch.Tensor          # (b,) fp32
     U: torch.Tensor | None     # (b, r) fp64
     Mc: torch.Tensor | None    # (r, r) fp64 Woodbury core: D = (g - U Mc U^T g) / rho
-    rho: float
+    rho: float                 # host value (nan on ranks that did not produce the batch)
     eta_dev: torch.Tensor      # (1,) fp64 view
     S: np.ndarray
     RAg: torch.Tensor | None = None  # (bpad, ka) gathered tensor-core row features
     eta_host: object = None          # () -> float: eta_t read back once its batch is produced
+    rho_dev: torch.Tensor | None = None  # (1,) fp64 view of rho on the device
 
 
 class _Slot:
@@ -79,6 +80,10 @@ class _Slot:
         self.Kbb = torch.zeros((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
+        # a batch's products, packed for the owner rank's broadcast (multi-GPU):
+        # [U (b r), Mc (r r), E (r), rho, eta, bad] per iteration
+        self.nprod = b * r + r * r + r + 3
+        self.prod = torch.empty((L, self.nprod), dtype=f64, device=dev)
         bpad = (b + 255) // 256 * 256
         self.RAg = torch.empty((L, bpad, ka), dtype=fdtype, device=dev) if ka else None
         pin = torch.cuda.is_available()
@@ -110,6 +115,7 @@ class _Batch:
     S: list
     ready: torch.cuda.Event = field(default=None)
     eta_ready: torch.cuda.Event = field(default=None)
+    owner: int = 0
 
 
 class Lookahead:
@@ -203,8 +209,9 @@ class Lookahead:
     def _submit(self, k):
         t0, t1 = self.bounds[k], self.bounds[k + 1]
         ns = len(self.slots)
+        owner = k % self.shard.world
         self.futs[k] = self.pool.submit(self._produce, self.slots[k % ns], t0, t1 - t0,
-                                        self.sides[k % ns])
+                                        self.sides[k % ns], owner)
 
     def close(self):
         self.pool.shutdown(wait=True)
@@ -225,6 +232,8 @@ class Lookahead:
             self.k += 1
             cur = self.futs.pop(self.k).result()
             main.wait_event(cur.ready)
+            if self.shard.world > 1:
+                self._share(cur)
             self.cur = cur
             if self.k + self.depth < len(self.bounds) - 1:
                 self._submit(self.k + self.depth)
@@ -241,7 +250,42 @@ class Lookahead:
             loc_dev=s.loc_dev[i], Xb=s.Xb[i], rsq=s.rsq[i],
             U=None if s.U is None else s.U[i], Mc=None if s.Mc is None else s.Mc[i],
             rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i],
-            RAg=None if s.RAg is None else s.RAg[i], eta_host=eta_host)
+            RAg=None if s.RAg is None else s.RAg[i], eta_host=eta_host,
+            rho_dev=s.rho[i:i + 1])
+
+    def _share(self, cur):
+        """Multi-GPU: batch k's Nystrom/stepsize products were computed by rank
+        k % world only (Phases II-III round-robin); one NCCL
+        broadcast of the packed products per batch, issued by every rank's main
+        thread in batch order, so collective order is identical on all ranks."""
+        s, n, b, r = cur.slot, cur.count, self.b, self.r
+        P = s.prod[:n]
+        owner = cur.owner == self.shard.rank
+        if owner:
+            o = 0
+            if r:
+                P[:, o:o + b * r].copy_(s.U[:n].reshape(n, b * r)); o += b * r
+                P[:, o:o + r * r].copy_(s.Mc[:n].reshape(n, r * r)); o += r * r
+                P[:, o:o + r].copy_(s.E[:n, :r]); o += r
+            else:
+                o = b * r + r * r + r
+            P[:, o].copy_(s.rho[:n]); P[:, o + 1].copy_(s.eta[:n])
+            P[:, o + 2].copy_(s.bad[:n].to(torch.float64))
+        torch.distributed.broadcast(P, src=cur.owner)
+        if not owner:
+            o = 0
+            if r:
+                s.U[:n].copy_(P[:, o:o + b * r].reshape(n, b, r)); o += b * r
+                s.Mc[:n].copy_(P[:, o:o + r * r].reshape(n, r, r)); o += r * r
+                s.E[:n, :r].copy_(P[:, o:o + r]); o += r
+            else:
+                o = b * r + r * r + r
+            s.rho[:n].copy_(P[:, o]); s.eta[:n].copy_(P[:, o + 1])
+            s.bad[:n] |= P[:, o + 2].to(torch.int32)
+            s.h_eta[:n].copy_(s.eta[:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.dev))
+            cur.eta_ready = ev
 
     def check_flags(self):
         """Raise if any power iteration or device normal draw failed (checked once,
@@ -254,7 +298,9 @@ class Lookahead:
                                      "estimate; H is not PSD)")
 
     # -- producer side (worker thread) ------------------------------------------
-    def _produce(self, slot, t0, count, side):
+    def _produce(self, slot, t0, count, side, owner=0):
+        if owner != self.shard.rank:
+            return self._produce_blocks(slot, t0, count, side, owner)
         b, r, seed, n = self.b, self.r, self.seed, self.n
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
@@ -380,7 +426,38 @@ class Lookahead:
         if self.timings is not None:
             self.timings.append(dict(count=count, rng=tm1 - tm0, gpu_wait=tm2 - tm1,
                                      factor=tm3 - tm2, total=time.perf_counter() - tm0))
-        return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready, eta_ready)
+        return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready, eta_ready, owner)
+
+    def _produce_blocks(self, slot, t0, count, side, owner):
+        """A batch another rank produces: only what this rank's Phase I/IV needs
+        locally (the blocks, their local rows and gathered features); the
+        products arrive by broadcast in get()."""
+        seed, n, b = self.seed, self.n, self.b
+        if slot.h2d_done is not None:
+            slot.h2d_done.synchronize()
+
+        def draw(i):
+            blk = uniform_block(seed, t0 + i, n, b).astype(np.int64)
+            slot.h_block[i].numpy()[:] = blk
+            return blk, block_hash(blk)
+
+        drawn = list(self.hostpool.map(draw, range(count)))
+        pts = self.o.points
+        with torch.cuda.device(self.dev), torch.cuda.stream(side):
+            if slot.free is not None:
+                side.wait_event(slot.free)
+            slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
+            bd = slot.block_dev[:count]
+            slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
+            for i in range(count):
+                pts.gather(bd[i], out=(slot.Xb[i], slot.rsq[i]))
+                if self.tcp is not None:
+                    self.tcp.gather_rows(bd[i], out=slot.RAg[i])
+            ready = torch.cuda.Event()
+            ready.record(side)
+            slot.h2d_done = ready
+        return _Batch(slot, t0, count, [d[0] for d in drawn], [d[1] for d in drawn],
+                      np.full(count, np.nan), [None] * count, ready, None, owner)
 
 
 class _Cols:

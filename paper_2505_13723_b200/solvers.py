@@ -388,9 +388,9 @@ class AdasapEngine:
         allreduce_sum_(self.g)
         # Phase IV: D_B = (g - U diag(Mc) U^T g) / rho
         if plan.U is not None:
-            D = (self.g - plan.U @ (plan.Mc @ (plan.U.T @ self.g))) / plan.rho
+            D = (self.g - plan.U @ (plan.Mc @ (plan.U.T @ self.g))) / plan.rho_dev
         else:
-            D = self.g / plan.rho
+            D = self.g / plan.rho_dev
         self._update(plan, D)
         self.etas[self.t:self.t + 1].copy_(plan.eta_dev)
         self.last_loc = plan.loc_dev
