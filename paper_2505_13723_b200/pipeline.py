@@ -359,10 +359,15 @@ class Lookahead:
                         K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
                                       sketch[i], col_ids=bd[i])
             if r:
-                Y = sketch.to(torch.float64)
-                omt = om.transpose(1, 2)
-                small = torch.stack([Y.transpose(1, 2) @ Y, omt @ Y, omt @ om], dim=1)
-                slot.h_small[:count].copy_(small, non_blocking=True)
+                # the three Gram matrices Y^T Y, Omega^T Y, Omega^T Omega as blocks
+                # of ONE batched product [Y Omega]^T [Y Omega] (one wide GEMM
+                # instead of three 100 x 100 ones)
+                YO = torch.cat([sketch.to(torch.float64), om], dim=2)
+                Y = YO[:, :, :r]
+                G = YO.transpose(1, 2) @ YO
+                slot.h_small[:count, 0].copy_(G[:, :r, :r], non_blocking=True)
+                slot.h_small[:count, 1].copy_(G[:, r:, :r], non_blocking=True)
+                slot.h_small[:count, 2].copy_(G[:, r:, r:], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(side)
         rho = np.empty(count)
