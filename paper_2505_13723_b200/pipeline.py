@@ -416,9 +416,18 @@ class Lookahead:
         # solver's stream, between two block-row products.
         with torch.cuda.device(self.dev), torch.cuda.stream(self.main):
             self.main.wait_event(inputs)
-            K.power_stepsize(slot.Kbb[:count], slot.U[:count] if r else None,
-                             slot.E[:count], slot.rho[:count], slot.v0[:count], self.lam,
-                             self.iters, slot.eta[:count], slot.bad[:count])
+            # SAP_POWER_L2=<bytes> splits the batch so each launch's K_BB blocks
+            # fit that budget and stay in L2 across the 10 power steps (alone:
+            # 71 us per iteration in launches of 4 against 86 us in one launch of
+            # 8; inside the solver no difference beyond run-to-run noise, so
+            # one launch by default)
+            budget = float(os.environ.get("SAP_POWER_L2", "1e12"))
+            step = max(1, min(count, int(budget // (4 * b * b))))
+            for q0 in range(0, count, step):
+                q1 = min(count, q0 + step)
+                K.power_stepsize(slot.Kbb[q0:q1], slot.U[q0:q1] if r else None,
+                                 slot.E[q0:q1], slot.rho[q0:q1], slot.v0[q0:q1], self.lam,
+                                 self.iters, slot.eta[q0:q1], slot.bad[q0:q1])
             ready = torch.cuda.Event()
             ready.record(self.main)
             slot.h2d_done = ready  # pinned host buffers reusable after this point
