@@ -133,7 +133,12 @@ class Lookahead:
         # config 3); SAP_LOOKAHEAD_DEPTH overrides
         self.depth = max(2, int(os.environ.get("SAP_LOOKAHEAD_DEPTH", "4")))
         # depth + 1 slots of L fp32 b x b blocks: keep them under ~4 GB
-        cap = max(1, int(4e9 // ((self.depth + 1) * 4 * b * b)))
+        # slots: depth in production + the one being consumed + SAP_SPARE_SLOTS
+        # (default 1): a batch's production first waits until its slot's
+        # previous batch has left the device; one spare slot makes that the
+        # batch before last, not the last one
+        self.nslots = self.depth + 1 + max(0, int(os.environ.get("SAP_SPARE_SLOTS", "1")))
+        cap = max(1, int(4e9 // (self.nslots * 4 * b * b)))
         self.total, self.L = total, max(1, min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
@@ -147,14 +152,24 @@ class Lookahead:
         # SAP_SIDE_STREAM=1 selects the side streams for experiments.
         self.main = torch.cuda.current_stream(dev)
         if os.environ.get("SAP_SIDE_STREAM", "0") == "1":
-            self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(self.depth + 1)]
+            self.sides = [torch.cuda.Stream(device=dev, priority=-1) for _ in range(self.nslots)]
         else:
-            self.sides = [torch.cuda.current_stream(dev)] * (self.depth + 1)
+            self.sides = [torch.cuda.current_stream(dev)] * self.nslots
+        # the first production phase (Omega, gathers, sketch, Gram matrices --
+        # what the producer waits for before its host factorisation) runs on a
+        # high-priority stream: on the solver's stream it sat behind every
+        # block product already queued (~7 ms of producer wait per iteration
+        # at lookahead depth 4); its kernels are short, so they slip in between
+        # two block products. SAP_FAST_STREAM=0 keeps it on the solver's stream.
+        if os.environ.get("SAP_FAST_STREAM", "1") == "1":
+            self.fast = torch.cuda.Stream(device=dev, priority=-1)
+        else:
+            self.fast = None
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
         fdt = tcp.dtype if tcp is not None else torch.float32
         self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka, fdt)
-                      for _ in range(self.depth + 1)]
+                      for _ in range(self.nslots)]
         # per-slot scratch of the tensor-core sketch (used one plan at a time by
         # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
@@ -328,9 +343,10 @@ class Lookahead:
         crcs = [d[1] for d in drawn]
         tm1 = time.perf_counter()
         pts = self.o.points
-        with torch.cuda.device(self.dev), torch.cuda.stream(side):
+        fs = self.fast if self.fast is not None else side
+        with torch.cuda.device(self.dev), torch.cuda.stream(fs):
             if slot.free is not None:
-                side.wait_event(slot.free)
+                fs.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
             slot.v0[:count].copy_(slot.h_v0[:count], non_blocking=True)
             om = None
@@ -363,13 +379,14 @@ class Lookahead:
                 # of ONE batched product [Y Omega]^T [Y Omega] (one wide GEMM
                 # instead of three 100 x 100 ones)
                 YO = torch.cat([sketch.to(torch.float64), om], dim=2)
+                YO.record_stream(side)  # Y is read again on the solver's stream below
                 Y = YO[:, :, :r]
                 G = YO.transpose(1, 2) @ YO
                 slot.h_small[:count, 0].copy_(G[:, :r, :r], non_blocking=True)
                 slot.h_small[:count, 1].copy_(G[:, r:, :r], non_blocking=True)
                 slot.h_small[:count, 2].copy_(G[:, r:, r:], non_blocking=True)
             ev = torch.cuda.Event()
-            ev.record(side)
+            ev.record(fs)
         rho = np.empty(count)
         tm2 = time.perf_counter()
         if r:
@@ -398,6 +415,7 @@ class Lookahead:
         tm3 = time.perf_counter()
         slot.h_rho[:count].numpy()[:] = rho
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
+            side.wait_event(ev)  # phase 1 (fast stream) done: Xb, rsq, Y
             for i in range(count):
                 Xb, rsq = slot.Xb[i], slot.rsq[i]
                 K.ktile_f32(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d,
@@ -457,9 +475,10 @@ class Lookahead:
 
         drawn = list(self.hostpool.map(draw, range(count)))
         pts = self.o.points
-        with torch.cuda.device(self.dev), torch.cuda.stream(side):
+        fs = self.fast if self.fast is not None else side
+        with torch.cuda.device(self.dev), torch.cuda.stream(fs):
             if slot.free is not None:
-                side.wait_event(slot.free)
+                fs.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
@@ -468,7 +487,7 @@ class Lookahead:
                 if self.tcp is not None:
                     self.tcp.gather_rows(bd[i], out=slot.RAg[i])
             ready = torch.cuda.Event()
-            ready.record(side)
+            ready.record(fs)
             slot.h2d_done = ready
         return _Batch(slot, t0, count, [d[0] for d in drawn], [d[1] for d in drawn],
                       np.full(count, np.nan), [None] * count, ready, None, owner)
