@@ -15,8 +15,11 @@ from paper_2505_13723_b200.solvers import AdasapEngine
 ap = argparse.ArgumentParser()
 ap.add_argument("--family", default="matern32")
 ap.add_argument("--steps", type=int, default=120)
+ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--d", type=int, default=9)
+ap.add_argument("--b", type=int, default=2000)
 a = ap.parse_args()
-n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
+n, d, b, m, r = a.n, a.d, a.b, 65, 100
 prob = synthetic.make_problem(n, d, a.family, m, seed=0, lam=1e-2, device="cuda", rhs="noise")
 o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
 cfg = sap.RunConfig(lam=prob.lam, blocksize=b, nystrom_rank=r, residual_every=0,
