@@ -16,10 +16,12 @@ threads, up to ``depth`` batches ahead of the block-row products that
 consume them; their GPU work is enqueued in order on the solver's stream
 (see Lookahead.__init__). Batch sizes ramp 1, 2, 4, ... up to
 ``L = config.lookahead`` so the first iteration waits for one plan only, not
-for a full batch. Per batch there is one device->host round trip (three
-r x r Gram matrices per iteration) for the host LAPACK part
-(``randnla.factor_gram_retry``); everything dimension-b runs on the GPU
-(Omega, the sketch, U = Y W, K[B,B], the batched power iteration). Buffers
+for a full batch. Per batch there is one device->host round trip: the r x r
+matrices whose symmetric eigensolves run on the host workers (LAPACK beats the
+GPU's batched eigensolver at r = 100); the rest of the factorisation (the
+shift ladder's Cholesky factors, the Woodbury core, rho) and everything
+dimension-b runs on the GPU (``randnla.factor_gram_batch``; Omega, the
+sketch, U = Y W, K[B,B], the batched power iteration). Buffers
 live in depth + 1 preallocated slots reused under CUDA events, so nothing is
 allocated in steady state.
 """
@@ -30,6 +32,7 @@ import math
 import os
 import sys
 import time
+import warnings
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -38,7 +41,8 @@ import torch
 
 from . import kernels as K
 from .errors import NumericalError
-from .randnla import factor_gram_retry, woodbury_core
+from .errors import ContractError
+from .randnla import FactorFailure, factor_gram_batch
 from .rng import DeviceNormals, block_hash, pcg64_words, substream, uniform_block
 
 
@@ -95,10 +99,6 @@ class _Slot:
         self.omega = torch.empty((L, b, r), dtype=f64, device=dev) if r else None
         self.normals = DeviceNormals(b * r, L, dev) if r else None
         self.h_v0 = torch.empty((L, b), dtype=f64, pin_memory=pin)
-        self.h_small = torch.empty((L, 3, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
-        self.h_w = torch.empty((L, 2, max(r, 1), max(r, 1)), dtype=f64, pin_memory=pin)
-        self.h_coef = torch.empty((L, max(r, 1)), dtype=f64, pin_memory=pin)
-        self.h_rho = torch.empty(L, dtype=f64, pin_memory=pin)
         self.h_eta = torch.empty(L, dtype=f64, pin_memory=pin)
         self.free = None      # event on the main stream: last consumer enqueued
         self.h2d_done = None  # event on the side stream: pinned inputs consumed
@@ -182,6 +182,14 @@ class Lookahead:
                 slot.sk_zop = K.ZOperand(self.r, b, dev)
                 slot.sk_cols = torch.empty((b, ka), dtype=fdt, device=dev)
                 slot.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
+        # torch.linalg's CUDA backends initialise lazily and not thread-safely:
+        # touch the ones the producers use here, before any producer runs
+        if self.r:
+            with torch.cuda.device(dev):
+                _a = torch.eye(2, dtype=torch.float64, device=dev)[None]
+                _l, _ = torch.linalg.cholesky_ex(_a)
+                torch.cholesky_inverse(_l)
+                torch.linalg.solve_triangular(_l, _a, upper=False)
         # batch k covers iterations [bounds[k], bounds[k+1])
         self.bounds = [0]
         c = 1
@@ -379,53 +387,50 @@ class Lookahead:
                 # of ONE batched product [Y Omega]^T [Y Omega] (one wide GEMM
                 # instead of three 100 x 100 ones)
                 YO = torch.cat([sketch.to(torch.float64), om], dim=2)
-                YO.record_stream(side)  # Y is read again on the solver's stream below
                 Y = YO[:, :, :r]
                 G = YO.transpose(1, 2) @ YO
-                slot.h_small[:count, 0].copy_(G[:, :r, :r], non_blocking=True)
-                slot.h_small[:count, 1].copy_(G[:, r:, :r], non_blocking=True)
-                slot.h_small[:count, 2].copy_(G[:, r:, r:], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(fs)
-        rho = np.empty(count)
+        rho = np.full(count, np.nan)  # host copy not needed: the device holds rho
         tm2 = time.perf_counter()
+        Ss = [None] * count
         if r:
-            ev.synchronize()
-            tm2 = time.perf_counter()
-            hs = slot.h_small[:count].numpy()
-            dom = slot.omega
-
-            def factor(i):
-                W, S, UtU = factor_gram_retry(hs[i, 0], hs[i, 1], hs[i, 2], r,
-                                              omega_rank=lambda: np.linalg.matrix_rank(
-                                                  dom[i].cpu().numpy()))
-                rho_i = float(S[-1]) + self.lam
-                slot.h_w[i, 0].numpy()[:] = W
-                slot.h_w[i, 1].numpy()[:] = woodbury_core(S, UtU, rho_i)
-                slot.h_coef[i].numpy()[:] = 1.0 / np.sqrt(S + rho_i) - 1.0 / math.sqrt(rho_i)
-                return rho_i, S
-
-            res = list(self.hostpool.map(factor, range(count)))
-            rho[:] = [x[0] for x in res]
-            Ss = [x[1] for x in res]
+            # the r x r factorisations, batched on the device (fast stream); only
+            # the symmetric eigensolves go to the host workers (one sync)
+            with torch.cuda.device(self.dev), torch.cuda.stream(fs):
+                def eigh_host(H):
+                    res = list(self.hostpool.map(np.linalg.eigh, H))
+                    return np.stack([x[0] for x in res]), np.stack([x[1] for x in res])
+                try:
+                    W, S, rho_d, Mc, E, plain = factor_gram_batch(
+                        G[:, :r, :r], G[:, r:, :r], G[:, r:, r:], r, self.lam, eigh_host)
+                except FactorFailure as exc:
+                    i = int(exc.args[0][0])
+                    if np.linalg.matrix_rank(slot.omega[i].cpu().numpy()) < r:
+                        raise ContractError("test matrix omega is rank deficient") from exc
+                    raise NumericalError("Cholesky of the shifted Gram failed at every shift") \
+                        from exc
+                tm2 = time.perf_counter()
+                torch.bmm(Y, W, out=slot.U[:count])
+                slot.Mc[:count].copy_(Mc)
+                slot.E[:count, :r].copy_(E)
+                slot.rho[:count].copy_(rho_d)
+                if bool(plain.any()):
+                    warnings.warn("stabilized Woodbury Cholesky failed; falling back to the plain "
+                                  "identity", RuntimeWarning)
+                ev = torch.cuda.Event()
+                ev.record(fs)
         else:
             ev.synchronize()  # pinned inputs consumed before the slot is refilled
-            rho[:] = 1.0
-            Ss = [np.zeros(0)] * count
+            with torch.cuda.device(self.dev):
+                slot.rho[:count].fill_(1.0)
         tm3 = time.perf_counter()
-        slot.h_rho[:count].numpy()[:] = rho
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
-            side.wait_event(ev)  # phase 1 (fast stream) done: Xb, rsq, Y
+            side.wait_event(ev)  # phase 1 (fast stream) done: Xb, rsq, U, Mc, E, rho
             for i in range(count):
                 Xb, rsq = slot.Xb[i], slot.rsq[i]
                 K.ktile_f32(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d,
                             slot.Kbb[i])
-            slot.rho[:count].copy_(slot.h_rho[:count], non_blocking=True)
-            if r:
-                w = slot.h_w[:count].to(self.dev, non_blocking=True)
-                torch.bmm(Y, w[:, 0], out=slot.U[:count])
-                slot.Mc[:count].copy_(w[:, 1])
-                slot.E[:count].copy_(slot.h_coef[:count], non_blocking=True)
             inputs = torch.cuda.Event()
             inputs.record(side)
         # The power iteration is one long cluster kernel on 128 SMs: on the side

@@ -127,3 +127,52 @@ def test_no_cpu_fallback_without_device(monkeypatch):
         pytest.skip("device present")
     with pytest.raises(sap.WorkerError):
         sap.KernelOracle(sap.KernelSpec("rbf", np.ones(2)), np.zeros((4, 2)), 0.1)
+
+
+def test_batched_device_factor_matches_host_factor():
+    """randnla.factor_gram_batch (the lookahead's batched factorisation; run here
+    on CPU tensors) equals the per-element host path factor_gram_retry +
+    woodbury_core + rho + the P^{-1/2} coefficients, including an element that
+    needs a shift escalation and one with pruned null modes."""
+    import torch
+    from paper_2505_13723_b200.randnla import (factor_gram_batch, factor_gram_retry,
+                                               woodbury_core)
+    rng = np.random.default_rng(4)
+    b, r, lam = 300, 40, 1e-2
+    trip = []
+    for case in range(4):
+        A = rng.standard_normal((b, b if case != 2 else 25))
+        M = A @ A.T / b                      # case 2: rank 25 < r (null modes)
+        Om = rng.standard_normal((b, r))
+        Y = M @ Om
+        if case == 3:                        # indefinite at the first shift
+            Y = Y - 1e-9 * np.abs(Y).max() * Om
+        trip.append((Y.T @ Y, Om.T @ Y, Om.T @ Om))
+    G = [torch.as_tensor(np.stack([t[k] for t in trip])) for k in range(3)]
+
+    def eigh_host(H):
+        return np.linalg.eigh(H)
+
+    W, S, rho, Mc, E, plain = factor_gram_batch(G[0], G[1], G[2], r, lam, eigh_host)
+    for i, (gyy, goy, goo) in enumerate(trip):
+        Wh, Sh, UtU = factor_gram_retry(gyy, goy, goo, r)
+        rho_h = float(Sh[-1]) + lam
+        Mch = woodbury_core(Sh, UtU, rho_h)
+        if i == 2:
+            # rank-deficient sketch: its shifted Gram is PD only up to rounding, so
+            # batched and unbatched LAPACK may settle on different shift levels;
+            # the retained modes agree, the null tail (S ~ 1e-5, far below rho)
+            # is rounding noise either way
+            top = Sh > 1e-3 * Sh.max()
+            np.testing.assert_allclose(S[i].numpy()[top], Sh[top], rtol=1e-6)
+            continue
+        np.testing.assert_allclose(S[i].numpy(), Sh, rtol=1e-9, atol=1e-12 * Sh.max())
+        assert abs(float(rho[i]) - rho_h) <= 1e-9 * rho_h
+        # eigenvectors are defined up to sign: compare the products that matter
+        np.testing.assert_allclose((W[i] @ W[i].T).numpy(), Wh @ Wh.T, rtol=1e-7,
+                                   atol=1e-9 * np.abs(Wh @ Wh.T).max())
+        np.testing.assert_allclose((W[i] @ Mc[i] @ W[i].T).numpy(), Wh @ Mch @ Wh.T, rtol=1e-6,
+                                   atol=1e-9 * np.abs(Wh @ Mch @ Wh.T).max())
+        np.testing.assert_allclose(E[i].numpy(), 1.0 / np.sqrt(Sh + rho_h) - 1.0 / np.sqrt(rho_h),
+                                   rtol=1e-8, atol=1e-12)
+    assert not plain.any()
