@@ -62,7 +62,10 @@ __device__ __forceinline__ unsigned long long prof_clock() {
 
 constexpr int NT = 128;     // points per column tile (64 staged per CTA)
 constexpr int NB = 3;       // S/P tiles in flight in TMEM (columns 0..383)
-constexpr int kSeg = 16;    // tiles per TMEM accumulator segment (2048 points)
+#ifndef SAP_KSEG
+#define SAP_KSEG 16
+#endif
+constexpr int kSeg = SAP_KSEG;  // tiles per TMEM accumulator segment (2048 points)
 constexpr uint32_t kGCol = NB * NT;  // the (single) accumulator, nz columns
 constexpr int kEpiGroups = 4;                       // epilogue warpgroups
 constexpr int kThreads = 128 * (1 + kEpiGroups);    // + the control warpgroup
