@@ -19,9 +19,6 @@
 
 #include "krows_tc.cuh"
 
-#ifndef SAP_EPI_PIPE
-#define SAP_EPI_PIPE 0
-#endif
 // per-role cycle timers (SAP_TC_PROF=1 at run time needs a -DSAP_TC_TIMERS=1
 // build); compiled out otherwise -- the clock reads cost epilogue issue slots
 #ifndef SAP_TC_TIMERS
@@ -378,48 +375,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
       }
     };
-#if SAP_EPI_PIPE
-    // P for 16 of this warp's 32 tile columns (entries e0..e0+15): o[0..7] the
-    // packed fp16 hi words, o[8..15] the lo words
-    auto convert16 = [&](const uint32_t(&v)[16], int e0, int dc, bool diag, uint32_t(&o)[16]) {
-      if (p.debug == 1) {  // profiling: tensor/TMEM pipeline without the epilogue math
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = v[e];
-      } else if (p.debug == 11) {  // profiling: split only, kernel value -> one FMUL
-#pragma unroll
-        for (int e = 0; e < 16; e += 2)
-          split2(__uint_as_float(v[e]) * 1.5f, __uint_as_float(v[e + 1]) * 1.5f, o[e / 2], o[8 + e / 2]);
-      } else if (p.debug == 12) {  // profiling: kernel value only, no fp16 split
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          o[e / 2] = __float_as_uint(pvalue<FAM>(__uint_as_float(v[e])));
-          o[8 + e / 2] = __float_as_uint(pvalue<FAM>(__uint_as_float(v[e + 1])));
-        }
-      } else if (p.debug == 13) {  // profiling: FMA-pipe exp2 everywhere
-#pragma unroll
-        for (int e = 0; e < 16; e += 2)
-          split2(pvalue<FAM, true>(__uint_as_float(v[e])), pvalue<FAM, true>(__uint_as_float(v[e + 1])),
-                 o[e / 2], o[8 + e / 2]);
-      } else if (__any_sync(0xffffffffu, diag)) {
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          float p0 = pvalue<FAM>(__uint_as_float(v[e]));
-          float p1 = pvalue<FAM>(__uint_as_float(v[e + 1]));
-          if (diag && dc == e0 + e) p0 = kPScale;
-          if (diag && dc == e0 + e + 1) p1 = kPScale;
-          split2(p0, p1, o[e / 2], o[8 + e / 2]);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          const float x0 = __uint_as_float(v[e]), x1 = __uint_as_float(v[e + 1]);
-          split2(poly_entry<FAM>(e0 + e) ? pvalue<FAM, true>(x0) : pvalue<FAM>(x0),
-                 poly_entry<FAM>(e0 + e + 1) ? pvalue<FAM, true>(x1) : pvalue<FAM>(x1),
-                 o[e / 2], o[8 + e / 2]);
-        }
-      }
-    };
-#endif
     for (int u = pair; u < units; u += npairs) {
       const int rt = u % p.row_tiles, split = u / p.row_tiles;
       int64_t t0, t1;
@@ -436,65 +391,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
       }
       int seg_j = 0;
-#if SAP_EPI_PIPE
-      // Software-pipelined conversion in 16-column chunks: the TMEM load of the
-      // next chunk (the next tile's first chunk across the tile boundary) is in
-      // flight while this chunk's MUFU work runs, so the four warps sharing a
-      // sub-partition keep the MUFU pipe fed instead of all stalling on tile
-      // loads and stores at the same time.
-      uint32_t va[16], vb[16], oa[16], ob[16];
-      if (t0 < t1) {
-        epi_wait(sfull0 + 8 * r, ph);
-        tc::fence_after();
-        tc::ld16(tmem + lane_off + r * NT + w * 32, va);
-        tc::wait_ld();
-      }
-      for (int64_t t = t0; t < t1; ++t) {
-        const uint32_t taddr = tmem + lane_off + r * NT + w * 32;
-        tc::ld16(taddr + 16, vb);
-        const int64_t dc64 = rid - (p.col_base + t * NT) - w * 32;
-        const bool diag = dc64 >= 0 && dc64 < 32;
-        const int dc = int(dc64);
-        convert16(va, 0, dc, diag, oa);
-        tc::wait_ld();
-        tc::st8(taddr, oa);            // hi of points 0..15   -> columns 0..7
-        tc::st8(taddr + 16, oa + 8);   // lo of points 0..15   -> columns 16..23 (S already loaded)
-        const bool more = t + 1 < t1;
-        const uint32_t rn = r + 1 == NB ? 0 : r + 1;
-        const uint32_t phn = r + 1 == NB ? ph ^ 1 : ph;
-        if (more) {
-          ce = prof_clock();
-          epi_wait(sfull0 + 8 * rn, phn);
-          es += prof_clock() - ce;
-          tc::fence_after();
-          tc::ld16(tmem + lane_off + rn * NT + w * 32, va);
-        }
-        convert16(vb, 16, dc, diag, ob);
-        tc::st8(taddr + 8, ob);        // hi of points 16..31  -> columns 8..15
-        tc::st8(taddr + 24, ob + 8);   // lo of points 16..31  -> columns 24..31
-        ce = prof_clock();
-        tc::wait_st();
-        tc::wait_ld();
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(pfull_leader + 8 * r);
-        r = rn;
-        ph = phn;
-        const unsigned long long ca = prof_clock();
-        ea += ca - ce;
-        if (pend) drain();
-        ed += prof_clock() - ca;
-        if (seg_j == kSeg - 1 || t + 1 == t1) {
-          pend = true;
-          pend_last = t + 1 == t1;
-          pend_live = live;
-          pend_dst = dst;
-          seg_j = 0;
-        } else {
-          ++seg_j;
-        }
-      }
-#else
       for (int64_t t = t0; t < t1; ++t) {
         ce = prof_clock();
         epi_wait(sfull0 + 8 * r, ph);
@@ -552,7 +448,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ++seg_j;
         }
       }
-#endif
     }
     if (pend) drain();
     if (p.prof && warp == 4 && lane == 0) {
