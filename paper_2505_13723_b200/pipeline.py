@@ -57,6 +57,7 @@ class IterPlan:
     rsq: torch.Tensor          # (b,) fp32
     U: torch.Tensor | None     # (b, r) fp64
     Mc: torch.Tensor | None    # (r, r) fp64 Woodbury core: D = (g - U Mc U^T g) / rho
+    UMc: torch.Tensor | None   # (b, r) fp64 U Mc (precomputed, one GEMM less per step)
     rho: float                 # host value (nan on ranks that did not produce the batch)
     eta_dev: torch.Tensor      # (1,) fp64 view
     S: np.ndarray
@@ -74,6 +75,7 @@ class _Slot:
         self.rsq = torch.empty((L, b), dtype=f32, device=dev)
         self.U = torch.empty((L, b, r), dtype=f64, device=dev) if r else None
         self.Mc = torch.empty((L, r, r), dtype=f64, device=dev) if r else None
+        self.UMc = torch.empty((L, b, r), dtype=f64, device=dev) if r else None  # U Mc
         self.E = torch.zeros((L, max(r, 1)), dtype=f64, device=dev)
         self.rho = torch.ones(L, dtype=f64, device=dev)
         self.v0 = torch.empty((L, b), dtype=f64, device=dev)
@@ -272,6 +274,7 @@ class Lookahead:
             t=t, block=cur.blocks[i], crc=cur.crcs[i], block_dev=s.block_dev[i],
             loc_dev=s.loc_dev[i], Xb=s.Xb[i], rsq=s.rsq[i],
             U=None if s.U is None else s.U[i], Mc=None if s.Mc is None else s.Mc[i],
+            UMc=None if s.UMc is None else s.UMc[i],
             rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i],
             RAg=None if s.RAg is None else s.RAg[i], eta_host=eta_host,
             rho_dev=s.rho[i:i + 1])
@@ -305,6 +308,8 @@ class Lookahead:
                 o = b * r + r * r + r
             s.rho[:n].copy_(P[:, o]); s.eta[:n].copy_(P[:, o + 1])
             s.bad[:n] |= P[:, o + 2].to(torch.int32)
+            if r:
+                torch.bmm(s.U[:n], s.Mc[:n], out=s.UMc[:n])
             s.h_eta[:n].copy_(s.eta[:n], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream(self.dev))
@@ -413,6 +418,7 @@ class Lookahead:
                 tm2 = time.perf_counter()
                 torch.bmm(Y, W, out=slot.U[:count])
                 slot.Mc[:count].copy_(Mc)
+                torch.bmm(slot.U[:count], Mc, out=slot.UMc[:count])
                 slot.E[:count, :r].copy_(E)
                 slot.rho[:count].copy_(rho_d)
                 if bool(plain.any()):

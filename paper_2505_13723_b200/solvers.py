@@ -322,6 +322,8 @@ class AdasapEngine:
         beta, gamma, alpha = accel.beta, accel.gamma, accel.alpha
         self.beta, self.gamma, self.alpha = beta, gamma, alpha
         self.u1, self.u2, self.lam2, self.dense = _basis(beta, alpha)
+        self._u1x, self._u1y = float(self.u1[0]), float(self.u1[1])
+        self._u2x, self._u2y = float(self.u2[0]), float(self.u2[1])
         self.s = self.s_prev = 1.0
         nl = self.shard.size
         self.ld = max(4, (nl + 3) // 4 * 4)
@@ -360,7 +362,7 @@ class AdasapEngine:
         """One ADASAP iteration; returns the host IterPlan (block, crc, rho)."""
         plan = self.la.get(self.t)
         sh = self.shard
-        zp, zq = self.M[1, 0], self.M[1, 1]
+        zp, zq = self._u1y, self.s * self._u2y
         if point is None:
             R, R2, ca, cb = self.P, self.Q, zp, zq
         else:
@@ -388,7 +390,7 @@ class AdasapEngine:
         allreduce_sum_(self.g)
         # Phase IV: D_B = (g - U diag(Mc) U^T g) / rho
         if plan.U is not None:
-            D = (self.g - plan.U @ (plan.Mc @ (plan.U.T @ self.g))) / plan.rho_dev
+            D = torch.addmm(self.g, plan.UMc, plan.U.T @ self.g, alpha=-1.0).div_(plan.rho_dev)
         else:
             D = self.g / plan.rho_dev
         self._update(plan, D)
@@ -408,8 +410,8 @@ class AdasapEngine:
 
     def _update(self, plan, D):
         beta, gamma, alpha = self.beta, self.gamma, self.alpha
-        delta = np.array([-gamma, -(1.0 - alpha)])
-        M = self.M
+        delta = (-gamma, -(1.0 - alpha))
+        M = ((self._u1x, self.s * self._u2x), (self._u1y, self.s * self._u2y))
         if self.dense:
             # degenerate T (repeated/zero second eigenvalue): apply T to every row
             self._pq(plan, D, M, 0.0, 0.0)
@@ -420,9 +422,13 @@ class AdasapEngine:
             self._pq(plan, D, M, delta[0], delta[1], wb=False)
             return
         s_next = self.lam2 * self.s
-        M_next = np.column_stack([self.u1, s_next * self.u2])
-        e = np.linalg.solve(M_next, delta)
-        self._pq(plan, D, M, e[0], e[1])
+        # e = M_next^{-1} delta, M_next = [[a, s b], [c, s d]] (2x2 closed form)
+        a, c = self._u1x, self._u1y
+        bb, dd = s_next * self._u2x, s_next * self._u2y
+        det = a * dd - bb * c
+        e0 = (delta[0] * dd - bb * delta[1]) / det
+        e1 = (a * delta[1] - c * delta[0]) / det
+        self._pq(plan, D, M, e0, e1)
         self.s_prev, self.s = self.s, s_next
         if abs(s_next) < RENORM_LO or abs(s_next) > RENORM_HI:
             self.Q.mul_(s_next)
@@ -434,7 +440,7 @@ class AdasapEngine:
     def _pq(self, plan, D, M, e0, e1, wb=True):
         nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
                  nat.ptr(plan.loc_dev), self.b, self.m, nat.ptr(D), D.stride(0),
-                 nat.ptr(plan.eta_dev), M[1, 0], M[1, 1], e0, e1,
+                 nat.ptr(plan.eta_dev), M[1][0], M[1][1], e0, e1,
                  nat.ptr(self.WB) if wb else None, self.WB.stride(0), nat.ptr(self.Pb),
                  nat.ptr(self.Qb), nat.stream_handle())
 
