@@ -254,6 +254,22 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
                     void *ws, size_t ws_bytes, void *stream);
 int *sap_normal_status(void *ws);
 
+/*
+ * Host-side draws of iterations t0 .. t0+count-1 (no GPU involved; replaces
+ * the per-iteration numpy draws of the reference, solvers.py:260-262 block,
+ * :250-251 crc, :384 Nystrom test-matrix stream, :395 power start vector,
+ * via rng.py:14-24 substreams). Per iteration i:
+ *   blocks[i*b .. i*b+b)   sorted substream(seed,"block",t).choice(n,b,replace=False)
+ *   crcs[i]                zlib.crc32 of those int64 bytes
+ *   omega_states[4*i ..]   PCG64 words of substream(seed,"omega",t) (NULL: skip)
+ *   v0[i*b .. i*b+b)       substream(seed,"power",t).standard_normal(b) / its norm
+ *                          (NULL: skip; SAP_ERR_NUMERICAL if zero twice)
+ * Bit-exact with numpy except v0's normalisation (sum-of-squares order).
+ * Runs on nthreads host threads without the Python GIL.
+ */
+int sap_host_draws(uint64_t seed, int64_t t0, int count, int64_t n, int64_t b, int64_t *blocks,
+                   uint32_t *crcs, int64_t *omega_states, double *v0, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,7 +43,7 @@ from . import kernels as K
 from .errors import NumericalError
 from .errors import ContractError
 from .randnla import FactorFailure, factor_gram_batch
-from .rng import DeviceNormals, block_hash, pcg64_words, substream, uniform_block
+from .rng import DeviceNormals
 
 
 @dataclass
@@ -125,7 +125,9 @@ class Lookahead:
 
     def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
                  tcp=None):
-        self.o, self.shard, self.seed = oracle, shard, seed
+        self.o, self.shard, self.seed = oracle, shard, int(seed)
+        if not 0 <= self.seed < 2**64:
+            raise ContractError("seed must be a non-negative integer below 2**64")
         self.n, self.b, self.r, self.lam = oracle.n, b, (0 if identity_precond else r), lam
         # batches produced concurrently (one producer thread each, depth + 1
         # slots): a producer spends most of a batch waiting -- for its sketch,
@@ -208,7 +210,8 @@ class Lookahead:
             cores = len(os.sched_getaffinity(0))
         except AttributeError:  # pragma: no cover
             cores = os.cpu_count() or 1
-        self.hostpool = ThreadPoolExecutor(max_workers=max(1, min(self.L, cores - 2, 8)),
+        self.host_threads = max(1, min(self.L, cores - 2, 8))
+        self.hostpool = ThreadPoolExecutor(max_workers=self.host_threads,
                                            thread_name_prefix="sap-host")
         self.timings = [] if os.environ.get("SAP_PROFILE") else None
         # The solver thread enqueues ~20 launches per iteration and must keep
@@ -216,8 +219,9 @@ class Lookahead:
         # between their numpy/LAPACK calls: with CPython's default 5 ms GIL
         # switch interval it can wait a whole interval for the GIL, longer than
         # an iteration's device time. 0.2 ms bounds that wait.
-        if sys.getswitchinterval() > 2e-4:
-            sys.setswitchinterval(2e-4)
+        swi = float(os.environ.get("SAP_SWITCH_INTERVAL", "2e-4"))
+        if sys.getswitchinterval() > swi:
+            sys.setswitchinterval(swi)
         # r x r LAPACK calls from several host workers: one BLAS thread each (the
         # reference pins BLAS to one thread for the same reason, __init__.py:16-22)
         try:
@@ -326,6 +330,20 @@ class Lookahead:
                                      "estimate; H is not PSD)")
 
     # -- producer side (worker thread) ------------------------------------------
+    def _host_draws(self, slot, t0, count, omega, v0):
+        """Iterations t0..t0+count-1: blocks, crcs, omega PCG64 words and power
+        start vectors written into the slot's pinned buffers by
+        ``sap_host_draws`` (numpy-exact, csrc/host_rng.cu; GIL released, on
+        the host workers' thread budget). Returns host copies of the blocks
+        (the pinned rows are refilled when the slot is reused) and the crcs."""
+        crcs = np.empty(count, dtype=np.uint32)
+        K.nat.call("sap_host_draws", self.seed, t0, count, self.n, self.b,
+                   slot.h_block.data_ptr(), crcs.ctypes.data,
+                   slot.h_states.data_ptr() if omega else None,
+                   slot.h_v0.data_ptr() if v0 else None, self.host_threads)
+        blocks = slot.h_block[:count].numpy().copy()
+        return list(blocks), [int(c) for c in crcs]
+
     def _produce(self, slot, t0, count, side, owner=0):
         if owner != self.shard.rank:
             return self._produce_blocks(slot, t0, count, side, owner)
@@ -334,26 +352,7 @@ class Lookahead:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
         tm0 = time.perf_counter()
 
-        def draw(i):
-            t = t0 + i
-            blk = uniform_block(seed, t, n, b).astype(np.int64)
-            slot.h_block[i].numpy()[:] = blk
-            if r:
-                slot.h_states[i].numpy()[:] = pcg64_words(substream(seed, "omega", t))
-            rng = substream(seed, "power", t)
-            v = rng.standard_normal(b)
-            nv = np.linalg.norm(v)
-            if nv == 0.0:
-                v = rng.standard_normal(b)
-                nv = np.linalg.norm(v)
-                if nv == 0.0:
-                    raise NumericalError("power iteration start vector is zero")
-            slot.h_v0[i].numpy()[:] = v / nv
-            return blk, block_hash(blk)
-
-        drawn = list(self.hostpool.map(draw, range(count)))
-        blocks = [d[0] for d in drawn]
-        crcs = [d[1] for d in drawn]
+        blocks, crcs = self._host_draws(slot, t0, count, omega=bool(r), v0=True)
         tm1 = time.perf_counter()
         pts = self.o.points
         fs = self.fast if self.fast is not None else side
@@ -479,12 +478,7 @@ class Lookahead:
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()
 
-        def draw(i):
-            blk = uniform_block(seed, t0 + i, n, b).astype(np.int64)
-            slot.h_block[i].numpy()[:] = blk
-            return blk, block_hash(blk)
-
-        drawn = list(self.hostpool.map(draw, range(count)))
+        blocks, crcs = self._host_draws(slot, t0, count, omega=False, v0=False)
         pts = self.o.points
         fs = self.fast if self.fast is not None else side
         with torch.cuda.device(self.dev), torch.cuda.stream(fs):
@@ -500,7 +494,7 @@ class Lookahead:
             ready = torch.cuda.Event()
             ready.record(fs)
             slot.h2d_done = ready
-        return _Batch(slot, t0, count, [d[0] for d in drawn], [d[1] for d in drawn],
+        return _Batch(slot, t0, count, blocks, crcs,
                       np.full(count, np.nan), [None] * count, ready, None, owner)
 
 
