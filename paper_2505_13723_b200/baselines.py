@@ -35,7 +35,7 @@ from .errors import ConfigError, ContractError, NumericalError
 from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
 from .parallel import allreduce_sum_, current_shard, gather_rows
 from .randnla import rand_nystrom_retry, woodbury_core
-from .rng import block_hash, standard_normal, substream, uniform_block
+from .rng import native_blocks, standard_normal, substream
 
 SDD_MOMENTUM = 0.9          # solvers.py:25
 DIVERGENCE_FACTOR = 1e6     # solvers.py:24
@@ -59,8 +59,8 @@ class BlockFeed:
         self._fill()
 
     def _draw(self, t):
-        blk = uniform_block(self.seed, t, self.n, self.b).astype(np.int64)
-        return blk, block_hash(blk)
+        blocks, crcs = native_blocks(self.seed, t, 1, self.n, self.b)
+        return blocks[0], crcs[0]
 
     def _fill(self):
         while self.next_t < self.total and len(self.futs) < self.ahead:

@@ -31,6 +31,20 @@ def uniform_block(seed, iteration, n, blocksize):
     return np.sort(rng.choice(n, size=blocksize, replace=False))
 
 
+def native_blocks(seed, t0, count, n, blocksize, threads=1):
+    """``uniform_block`` and ``block_hash`` for iterations t0..t0+count-1 in one
+    native call (csrc/host_rng.cu, numpy-exact, GIL released): ((count, b)
+    int64 blocks, list of crcs)."""
+    import ctypes
+    from . import _native as nat
+    blocks = np.empty((count, blocksize), dtype=np.int64)
+    crcs = np.empty(count, dtype=np.uint32)
+    nat.call("sap_host_draws", int(seed), int(t0), int(count), int(n), int(blocksize),
+             blocks.ctypes.data_as(ctypes.c_void_p), crcs.ctypes.data_as(ctypes.c_void_p),
+             None, None, int(threads))
+    return blocks, [int(c) for c in crcs]
+
+
 def block_hash(block):
     """crc32 of the index bytes, the trace's cross-implementation check
     (solvers.py:250-251)."""

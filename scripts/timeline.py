@@ -10,12 +10,15 @@ from paper_2505_13723_b200.solvers import AdasapEngine
 n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
 prob = synthetic.make_problem(n, d, os.environ.get("FAM", "matern32"), m, seed=0, lam=1e-2, device="cuda", rhs="noise")
 o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
-cfg = sap.RunConfig(lam=prob.lam, blocksize=b, nystrom_rank=r, residual_every=0, max_iters=80)
-eng = AdasapEngine(o, prob.Y, cfg, sap.resolve_accel(cfg, n, b), total=80)
-for _ in range(16): eng.step()
+WARM, NIT = int(os.environ.get("WARM", "64")), int(os.environ.get("NIT", "64"))
+TOTAL = int(os.environ.get("TOTAL", str(WARM + NIT)))  # > WARM + NIT: production in the window
+cfg = sap.RunConfig(lam=prob.lam, blocksize=b, nystrom_rank=r, residual_every=0,
+                    max_iters=TOTAL)
+eng = AdasapEngine(o, prob.Y, cfg, sap.resolve_accel(cfg, n, b), total=TOTAL)
+for _ in range(WARM): eng.step()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    for _ in range(24): eng.step()
+    for _ in range(NIT): eng.step()
     torch.cuda.synchronize()
 eng.close()
 path = "/tmp/trace.json"
@@ -31,17 +34,27 @@ for i, e in enumerate(ev):
     busy += max(0.0, f - max(s, cur_end))
     cur_end = max(cur_end, f)
 span = t1 - t0
-print(f"span {span/24:.1f} us/iter, busy {busy/24:.1f} us/iter ({100*busy/span:.1f}%), kernels {len(ev)}")
+print(f"span {span/NIT:.1f} us/iter, busy {busy/NIT:.1f} us/iter ({100*busy/span:.1f}%), kernels {len(ev)}")
 gaps.sort(reverse=True)
 tot = sum(g[0] for g in gaps)
-print(f"idle {tot/24:.1f} us/iter in {len(gaps)} gaps; largest:")
+print(f"idle {tot/NIT:.1f} us/iter in {len(gaps)} gaps; largest:")
 for g in gaps[:15]:
     print(f"  {g[0]:8.1f} us  after {g[1]!r}  before {g[2]!r}")
 streams = {}
 for e in ev:
     streams.setdefault(e["args"].get("stream"), []).append(e)
 for sid, es in streams.items():
-    print(f"stream {sid}: {len(es)} kernels, {sum(e['dur'] for e in es)/24:.1f} us/iter")
+    print(f"stream {sid}: {len(es)} kernels, {sum(e['dur'] for e in es)/NIT:.1f} us/iter")
 # krows kernels: duration stats
 kr = [e["dur"] for e in ev if "krows_tc2_kernel<1, 80" in e["name"]]
-print("krows us:", [round(x) for x in kr[:24]])
+print("krows us:", [round(x) for x in kr[:NIT]])
+# per-kernel totals per iteration, by stream
+agg = {}
+for e in ev:
+    k = (e["args"].get("stream"), e["name"][:70])
+    a = agg.setdefault(k, [0, 0.0])
+    a[0] += 1
+    a[1] += e["dur"]
+print("per-iteration kernel time by stream (us/iter, launches/iter):")
+for (sid, name), (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(os.environ.get("TOPK", "40"))]:
+    print(f"  s{sid} {t/NIT:8.1f} us  {c/NIT:5.2f}x  {name}")

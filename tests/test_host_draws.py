@@ -90,3 +90,12 @@ def test_draws_contract_errors():
     p = (lambda a: a.ctypes.data_as(ctypes.c_void_p))
     with pytest.raises(nat.ContractError):
         nat.check(lib.sap_host_draws(0, 0, 1, 4, 8, p(buf), p(crc), None, None, 1))
+
+
+def test_native_blocks_helper():
+    from paper_2505_13723_b200.rng import native_blocks
+    _lib()
+    blocks, crcs = native_blocks(5, 3, 4, 7000, 300, threads=2)
+    for i in range(4):
+        ref = uniform_block(5, 3 + i, 7000, 300).astype(np.int64)
+        assert np.array_equal(blocks[i], ref) and crcs[i] == zlib.crc32(ref.tobytes())
