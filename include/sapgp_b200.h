@@ -121,6 +121,19 @@ int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, i
                   void *stream);
 
 /*
+ * K_BB of `count` blocks in one launch (the lookahead's power-iteration
+ * input; replaces count x oracle.block, kernels.py:129-136): block q's scaled
+ * points X + q*strideX ([b][ldx] fp32, sap_gather_points' layout) and squared
+ * norms xsq + q*strideSq against themselves into out + q*strideOut ([b][ldo]
+ * fp32, ldo and strideOut multiples of 4, 16-byte aligned), variance on the
+ * diagonal. The values of sap_ktile_f32 with row_ids = col_ids = the block's
+ * (unique) ids, bit for bit. d <= 64.
+ */
+int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64_t strideSq,
+                        int b, int count, int ldx, int d, int family, double variance, float *out,
+                        int64_t ldo, int64_t strideOut, void *stream);
+
+/*
  * Batched preconditioned power-iteration stepsize (replaces randnla.py:165-196
  * rand_power_stepsize, called at solvers.py:389-396), for `count` independent
  * problems q: H_q = P^{-1/2}(K_q + lam I)P^{-1/2} with

@@ -114,6 +114,72 @@ __global__ void __launch_bounds__(256)
 }
 
 
+// K_BB of a batch of blocks in one launch (the lookahead's power-iteration
+// input): block q's points X_q [b][ldx] (scaled fp32) against themselves,
+// 64x64 outputs per CTA of 256 threads, 4x4 per thread from [k][64] staged
+// coordinates (16-byte shared loads), 16-byte stores. The arithmetic is
+// ktile_kernel's (same fma order, same sum of norms, the id rule on the
+// diagonal: the block's ids are unique, so i == j), so the values are the
+// same bit for bit; ~5x faster than the 32x32 tiles at b = 2000.
+template <int FAM>
+__global__ void __launch_bounds__(256)
+    ktile_batch_kernel(const float *X, int64_t strideX, const float *xsq, int64_t strideSq, int b,
+                       int ldx, int d, float variance, float *out, int64_t ldo,
+                       int64_t strideOut) {
+  extern __shared__ __align__(16) float sh[];
+  float *sA = sh;            // [d][64] row points
+  float *sC = sh + d * 64;   // [d][64] column points
+  const int q = blockIdx.z;
+  const float *Xq = X + int64_t(q) * strideX;
+  const float *sq = xsq + int64_t(q) * strideSq;
+  float *oq = out + int64_t(q) * strideOut;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int e = tid; e < 64 * d; e += 256) {
+    const int r = e / d, k = e - r * d;
+    sA[k * 64 + r] = i0 + r < b ? Xq[int64_t(i0 + r) * ldx + k] : 0.0f;
+    sC[k * 64 + r] = j0 + r < b ? Xq[int64_t(j0 + r) * ldx + k] : 0.0f;
+  }
+  __syncthreads();
+  float dot[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dot[a][c] = 0.0f;
+  for (int k = 0; k < d; ++k) {
+    const float4 ra = *reinterpret_cast<const float4 *>(sA + k * 64 + ty * 4);
+    const float4 rc = *reinterpret_cast<const float4 *>(sC + k * 64 + tx * 4);
+    const float av[4] = {ra.x, ra.y, ra.z, ra.w}, cv[4] = {rc.x, rc.y, rc.z, rc.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dot[a][c] = fmaf(av[a], cv[c], dot[a][c]);
+  }
+  const int j = j0 + tx * 4;
+  float csq[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) csq[c] = j + c < b ? sq[j + c] : 0.0f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = i0 + ty * 4 + a;
+    if (i >= b) break;
+    const float rs = sq[i];
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      v[c] = (i == j + c) ? variance
+                          : variance * kernel_value<FAM>(fmaf(-2.0f, dot[a][c], rs + csq[c]));
+    float *o = oq + int64_t(i) * ldo + j;
+    if (j + 3 < b) {
+      *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (j + c < b) o[c] = v[c];
+    }
+  }
+}
+
 // fp64 tile for the dense-access API (KernelOracle.tile/block/dense,
 // kernels.py:118-143): the reference's own arithmetic -- z = x / l in fp64,
 // sq = |z_r|^2 + |z_c|^2 - 2 z_r.z_c, sq = 0 where the ids match, clamp at 0,
@@ -493,6 +559,35 @@ int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, i
                   void *stream) {
   return ktile_launch(Ra, rasqn, row_ids, na, Rc, rcsqn, col_ids, nc, ldx, d, family, variance,
                       out, ldo, stream);
+}
+
+int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64_t strideSq,
+                        int b, int count, int ldx, int d, int family, double variance, float *out,
+                        int64_t ldo, int64_t strideOut, void *stream) {
+  if (b <= 0 || count <= 0 || ldx < d || d < 1 || d > 64 || ldo < b || ldo % 4 ||
+      strideOut % 4 || (reinterpret_cast<uintptr_t>(out) & 15))
+    return fail(SAP_ERR_CONTRACT, "ktile_f32_batch: bad shape b=%d d=%d ldo=%lld", b, d,
+                (long long)ldo);
+  dim3 grid(unsigned((b + 63) / 64), unsigned((b + 63) / 64), unsigned(count));
+  const size_t smem = size_t(2 * 64 * d) * sizeof(float);
+  cudaStream_t st = S(stream);
+  const float var = float(variance);
+  switch (family) {
+    case SAP_RBF:
+      ktile_batch_kernel<SAP_RBF><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b, ldx, d,
+                                                           var, out, ldo, strideOut);
+      break;
+    case SAP_MATERN32:
+      ktile_batch_kernel<SAP_MATERN32><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b,
+                                                                ldx, d, var, out, ldo, strideOut);
+      break;
+    case SAP_MATERN52:
+      ktile_batch_kernel<SAP_MATERN52><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b,
+                                                                ldx, d, var, out, ldo, strideOut);
+      break;
+    default: return fail(SAP_ERR_CONTRACT, "ktile_f32_batch: unknown family %d", family);
+  }
+  return check_launch("ktile_batch_kernel");
 }
 
 int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q, const float *Y,

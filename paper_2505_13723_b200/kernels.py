@@ -273,6 +273,16 @@ def ktile_f32(spec, A, asq, aid, C, csq, cid, ldx, d, out):
     return out
 
 
+def ktile_f32_batch(spec, X, xsq, d, out):
+    """K_BB of each block in a batch (X: (count, b, ldx), xsq: (count, b)) into
+    out (count, b, ldo) fp32 in one launch: ktile_f32's values, bit for bit."""
+    count, b, ldx = X.shape
+    nat.call("sap_ktile_f32_batch", nat.ptr(X), X.stride(0), nat.ptr(xsq), xsq.stride(0), b,
+             count, ldx, d, spec.code, spec.variance, nat.ptr(out), out.stride(1), out.stride(0),
+             nat.stream_handle())
+    return out
+
+
 def power_stepsize(Kbb, U, E, rho, v0, lam, iters, eta, bad):
     """Batched preconditioned power iteration (randnla.py:165-196) over the
     leading ``Kbb.shape[0]`` problems: eta[q] = 1/(v.Hv), bad[q] |= failure."""

@@ -432,10 +432,8 @@ class Lookahead:
         tm3 = time.perf_counter()
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
             side.wait_event(ev)  # phase 1 (fast stream) done: Xb, rsq, U, Mc, E, rho
-            for i in range(count):
-                Xb, rsq = slot.Xb[i], slot.rsq[i]
-                K.ktile_f32(self.o.spec, Xb, rsq, bd[i], Xb, rsq, bd[i], pts.ldx, pts.d,
-                            slot.Kbb[i])
+            K.ktile_f32_batch(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
+                              slot.Kbb[:count])
             inputs = torch.cuda.Event()
             inputs.record(side)
         # The power iteration is one long cluster kernel on 128 SMs: on the side
