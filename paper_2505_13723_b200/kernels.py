@@ -207,6 +207,17 @@ class TcPoints:
             out.copy_(dst)
         return out
 
+    def gather_rows_batch(self, idx2d, out):
+        """Row-form features of a batch of blocks (idx2d: (count, b)) into
+        out[:, :b] ((count, bpad, ka) in the kernel's dtype; the pad rows
+        b..bpad are the caller's, zero): one gather and one copy per batch."""
+        count, b = idx2d.shape
+        dst = self._scratch(count * b)
+        nat.call("sap_tc_gather_rows", nat.ptr(self.RA), self.ka, nat.ptr(idx2d), count * b,
+                 count * b, nat.ptr(dst), nat.stream_handle())
+        out[:, :b].copy_(dst.view(count, b, self.ka))
+        return out
+
     def gather_rows(self, idx_dev, out=None):
         b = idx_dev.numel()
         bpad = (b + 255) // 256 * 256  # whole 256-row tiles of the CTA-pair kernel

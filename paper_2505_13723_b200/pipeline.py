@@ -91,7 +91,8 @@ class _Slot:
         self.nprod = b * r + r * r + r + 3
         self.prod = torch.empty((L, self.nprod), dtype=f64, device=dev)
         bpad = (b + 255) // 256 * 256
-        self.RAg = torch.empty((L, bpad, ka), dtype=fdtype, device=dev) if ka else None
+        # pad rows b..bpad zero once (the batched gather writes rows < b only)
+        self.RAg = torch.zeros((L, bpad, ka), dtype=fdtype, device=dev) if ka else None
         pin = torch.cuda.is_available()
         self.h_block = torch.empty((L, b), dtype=i64, pin_memory=pin)
         # Omega_t is drawn on the GPU from the omega stream's PCG64 state
@@ -184,7 +185,8 @@ class Lookahead:
             need = K.nat.load().sap_krows_tc_workspace(b, self.r, b)
             for slot in self.slots:
                 slot.sk_zop = K.ZOperand(self.r, b, dev)
-                slot.sk_cols = torch.empty((b, ka), dtype=fdt, device=dev)
+                slot.sk_cols = torch.empty((self.L, b, ka), dtype=fdt, device=dev)
+                slot.sk_bound = torch.empty(self.L * self.r, dtype=torch.float32, device=dev)
                 slot.sk_ws = torch.empty(need // 4 + 1, dtype=torch.float32, device=dev)
         # torch.linalg's CUDA backends initialise lazily and not thread-safely:
         # touch the ones the producers use here, before any producer runs
@@ -369,22 +371,30 @@ class Lookahead:
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
             sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
-            for i in range(count):
-                Xb, rsq = pts.gather(bd[i], out=(slot.Xb[i], slot.rsq[i]))
-                if self.tcp is not None:
-                    self.tcp.gather_rows(bd[i], out=slot.RAg[i])
-                if r:
-                    omc = om[i].T.to(torch.float32).contiguous()  # (r, b) column-major RHS
+            # the batch's gathers, feature conversions and column bounds in one
+            # launch each; per iteration only the sketch's Z operand and product
+            flat = bd.reshape(-1)
+            pts.gather(flat, out=(slot.Xb[:count].view(-1, pts.ldx), slot.rsq[:count].view(-1)))
+            if self.tcp is not None:
+                self.tcp.gather_rows_batch(bd, slot.RAg[:count])
+            if r:
+                omc = om.transpose(1, 2).to(torch.float32).contiguous()  # (count, r, b) RHS
+                if self.tc_sketch:
+                    # K[B,B] Omega on the tensor cores: the block's own points as
+                    # columns, rows matched to columns by block position
+                    cols = slot.sk_cols[:count]
+                    self.tcp.gather_cols(flat, out=cols.view(-1, cols.shape[2]))
+                    bound = slot.sk_bound[:count * r]
+                    K.nat.call("sap_colabsmax", K.nat.ptr(omc), b, b, count * r,
+                               K.nat.ptr(bound), K.nat.stream_handle())
+                for i in range(count):
                     if self.tc_sketch:
-                        # K[B,B] Omega on the tensor cores: the block's own points
-                        # as columns, rows matched to columns by block position
-                        self.tcp.gather_cols(bd[i], out=slot.sk_cols)
-                        slot.sk_zop.fill(omc)
+                        slot.sk_zop.fill(omc[i], Pb=bound[i * r:(i + 1) * r])
                         K.krows_tc(self.o.spec, self.tcp, slot.RAg[i], b, self.sk_pos,
-                                   slot.sk_zop, sketch[i], ws=slot.sk_ws,
-                                   cols=(slot.sk_cols, 0))
+                                   slot.sk_zop, sketch[i], ws=slot.sk_ws, cols=(cols[i], 0))
                     else:
-                        K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc,
+                        Xb, rsq = slot.Xb[i], slot.rsq[i]
+                        K.krows_times(self.o.spec, _Cols(pts, Xb, rsq), Xb, rsq, bd[i], omc[i],
                                       sketch[i], col_ids=bd[i])
             if r:
                 # the three Gram matrices Y^T Y, Omega^T Y, Omega^T Omega as blocks
