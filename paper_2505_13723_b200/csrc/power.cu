@@ -153,12 +153,27 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   // out_i = x_i / sqrt(rho) + U[i,:] . coef on own rows: each thread owns rows
   // tid, tid + kThreads, ... (U rows from shared memory; a thread's dot is
   // sequential in k, the same order for every row)
-  auto apply_u = [&](const double *x, double *out) {
-    for (int i = tid; i < nloc; i += kThreads) {
-      double s = 0.0;
+  // U[i,:] . coef with kSplit threads per row (adjacent lanes, each a
+  // contiguous quarter of k, combined by a fixed shuffle tree): four times
+  // shorter fp64 dependency chains than one thread per row
+  constexpr int kSplit = 4;
+  const int kq = (r + kSplit - 1) / kSplit, part_id = tid % kSplit;
+  auto row_dot = [&](int i) {
+    double s = 0.0;
+    if (i < nloc) {
       const double *ur = U + i * r;
-      for (int k = 0; k < r; ++k) s = fma(ur[k], coef[k], s);
-      out[i] = fma(x[i], isr, s);
+      const int k1 = min(r, (part_id + 1) * kq);
+      for (int k = part_id * kq; k < k1; ++k) s = fma(ur[k], coef[k], s);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    return s;
+  };
+  auto apply_u = [&](const double *x, double *out) {
+    for (int i0 = 0; i0 < nloc; i0 += kThreads / kSplit) {
+      const int i = i0 + tid / kSplit;
+      const double s = row_dot(i);
+      if (part_id == 0 && i < nloc) out[i] = fma(x[i], isr, s);
     }
     __syncthreads();
   };
@@ -225,14 +240,15 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
     if (r) ut_times(zloc);
     PP(4);
     double dvy = 0.0, dyy = 0.0;
-    for (int i = tid; i < nloc; i += kThreads) {
-      double s = 0.0;
-      const double *ur = U + i * r;
-      for (int k = 0; k < r; ++k) s = fma(ur[k], coef[k], s);
-      const double y = fma(zloc[i], isr, s);
-      dvy = fma(vloc[i], y, dvy);
-      dyy = fma(y, y, dyy);
-      zloc[i] = y;
+    for (int i0 = 0; i0 < nloc; i0 += kThreads / kSplit) {
+      const int i = i0 + tid / kSplit;
+      const double s = r ? row_dot(i) : 0.0;
+      if (part_id == 0 && i < nloc) {
+        const double y = fma(zloc[i], isr, s);
+        dvy = fma(vloc[i], y, dvy);
+        dyy = fma(y, y, dyy);
+        zloc[i] = y;
+      }
     }
     PP(5);
     block_sum2(dvy, dyy, red);

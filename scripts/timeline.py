@@ -51,7 +51,7 @@ print("krows us:", [round(x) for x in kr[:NIT]])
 # per-kernel totals per iteration, by stream
 agg = {}
 for e in ev:
-    k = (e["args"].get("stream"), e["name"][:70])
+    k = (e["args"].get("stream"), e["name"][:int(os.environ.get("NAMEW", "70"))])
     a = agg.setdefault(k, [0, 0.0])
     a[0] += 1
     a[1] += e["dur"]
