@@ -64,6 +64,9 @@ class IterPlan:
     RAg: torch.Tensor | None = None  # (bpad, ka) gathered tensor-core row features
     eta_host: object = None          # () -> float: eta_t read back once its batch is produced
     rho_dev: torch.Tensor | None = None  # (1,) fp64 view of rho on the device
+    eta_rho_dev: torch.Tensor | None = None  # (1,) eta / rho: the update of an unscaled D
+    batch_t0: int = -1                   # first iteration of this plan's lookahead batch
+    batch_eta: torch.Tensor | None = None  # the batch's stepsizes (device)
 
 
 class _Slot:
@@ -85,6 +88,7 @@ class _Slot:
         # columns (times a zero w); never-written pad bits must not be NaN
         self.Kbb = torch.zeros((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.eta = torch.empty(L, dtype=f64, device=dev)
+        self.eta_rho = torch.empty(L, dtype=f64, device=dev)  # eta / rho (Phase IV's 1/rho folded)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
         # a batch's products, packed for the owner rank's broadcast (multi-GPU):
         # [U (b r), Mc (r r), E (r), rho, eta, bad] per iteration
@@ -283,7 +287,8 @@ class Lookahead:
             UMc=None if s.UMc is None else s.UMc[i],
             rho=float(cur.rho[i]), eta_dev=s.eta[i:i + 1], S=cur.S[i],
             RAg=None if s.RAg is None else s.RAg[i], eta_host=eta_host,
-            rho_dev=s.rho[i:i + 1])
+            rho_dev=s.rho[i:i + 1], eta_rho_dev=s.eta_rho[i:i + 1], batch_t0=cur.t0,
+            batch_eta=s.eta[:cur.count])
 
     def _share(self, cur):
         """Multi-GPU: batch k's Nystrom/stepsize products were computed by rank
@@ -313,6 +318,7 @@ class Lookahead:
             else:
                 o = b * r + r * r + r
             s.rho[:n].copy_(P[:, o]); s.eta[:n].copy_(P[:, o + 1])
+            torch.div(s.eta[:n], s.rho[:n], out=s.eta_rho[:n])
             s.bad[:n] |= P[:, o + 2].to(torch.int32)
             if r:
                 torch.bmm(s.U[:n], s.Mc[:n], out=s.UMc[:n])
@@ -464,6 +470,7 @@ class Lookahead:
                 K.power_stepsize(slot.Kbb[q0:q1], slot.U[q0:q1] if r else None,
                                  slot.E[q0:q1], slot.rho[q0:q1], slot.v0[q0:q1], self.lam,
                                  self.iters, slot.eta[q0:q1], slot.bad[q0:q1])
+            torch.div(slot.eta[:count], slot.rho[:count], out=slot.eta_rho[:count])
             ready = torch.cuda.Event()
             ready.record(self.main)
             slot.h2d_done = ready  # pinned host buffers reusable after this point

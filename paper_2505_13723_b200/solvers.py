@@ -388,13 +388,15 @@ class AdasapEngine:
                  nat.ptr(plan.loc_dev), self.b, self.m, self.lam, nat.ptr(self.g),
                  self.g.stride(0), nat.stream_handle())
         allreduce_sum_(self.g)
-        # Phase IV: D_B = (g - U diag(Mc) U^T g) / rho
+        # Phase IV: D_B = (g - U Mc U^T g) / rho; the 1/rho rides on the
+        # update's stepsize (every use of D in sap_pq_update is eta * D)
         if plan.U is not None:
-            D = torch.addmm(self.g, plan.UMc, plan.U.T @ self.g, alpha=-1.0).div_(plan.rho_dev)
+            D = torch.addmm(self.g, plan.UMc, plan.U.T @ self.g, alpha=-1.0)
         else:
-            D = self.g / plan.rho_dev
+            D = self.g
         self._update(plan, D)
-        self.etas[self.t:self.t + 1].copy_(plan.eta_dev)
+        if self.t == plan.batch_t0:  # the batch's stepsizes into the trace, once per batch
+            self.etas[self.t:self.t + plan.batch_eta.numel()].copy_(plan.batch_eta)
         self.last_loc = plan.loc_dev
         self.crcs.append(plan.crc)
         self.t += 1
@@ -440,7 +442,7 @@ class AdasapEngine:
     def _pq(self, plan, D, M, e0, e1, wb=True):
         nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
                  nat.ptr(plan.loc_dev), self.b, self.m, nat.ptr(D), D.stride(0),
-                 nat.ptr(plan.eta_dev), M[1][0], M[1][1], e0, e1,
+                 nat.ptr(plan.eta_rho_dev), M[1][0], M[1][1], e0, e1,
                  nat.ptr(self.WB) if wb else None, self.WB.stride(0), nat.ptr(self.Pb),
                  nat.ptr(self.Qb), nat.stream_handle())
 

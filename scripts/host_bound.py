@@ -18,7 +18,7 @@ ap.add_argument("--steps", type=int, default=120)
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--d", type=int, default=9)
 ap.add_argument("--b", type=int, default=2000)
-ap.add_argument("--L", type=int, default=8)
+ap.add_argument("--L", type=int, default=32)
 a = ap.parse_args()
 n, d, b, m, r = a.n, a.d, a.b, 65, 100
 prob = synthetic.make_problem(n, d, a.family, m, seed=0, lam=1e-2, device="cuda", rhs="noise")
