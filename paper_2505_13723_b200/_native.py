@@ -82,11 +82,18 @@ def load():
         raise WorkerError(
             f"CUDA library {LIB_PATH} is not built; run __graft_entry__.build() "
             "(there is no CPU fallback)")
-    lib = ctypes.CDLL(LIB_PATH)  # calls release the GIL (sap_host_draws relies on it)
+    # SAP_PYDLL=1: the launch wrappers are called with the GIL held (they return
+    # in microseconds; releasing the GIL around each lets a producer thread in
+    # for up to a switch interval); sap_host_draws always releases it
+    pydll = os.environ.get("SAP_PYDLL", "0") == "1"
+    lib = (ctypes.PyDLL if pydll else ctypes.CDLL)(LIB_PATH)
+    free = ctypes.CDLL(LIB_PATH) if pydll else lib
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(free if name == "sap_host_draws" else lib, name)
         fn.restype = res
         fn.argtypes = args
+        if pydll and name == "sap_host_draws":
+            setattr(lib, name, fn)
     if lib.sap_abi_version() != ABI_VERSION:
         raise WorkerError("libsapgp_b200.so ABI version mismatch; rebuild")
     _lib = lib
