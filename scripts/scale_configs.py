@@ -26,7 +26,7 @@ import paper_2505_13723_b200 as sap  # noqa: E402
 import paper_2505_13723_b200.solvers as S  # noqa: E402
 from paper_2505_13723_b200.solvers import AdasapEngine  # noqa: E402
 
-CONFIGS = {2: dict(n=100_000, d=11, b=1000, warm=20, steps=200),
+CONFIGS = {2: dict(n=100_000, d=11, b=1000, warm=100, steps=2000),
            4: dict(n=10_000_000, d=9, b=5000, warm=6, steps=20),
            5: dict(n=100_000_000, d=9, b=10000, warm=3, steps=6)}
 m, r, lam = 65, 100, 1e-2
