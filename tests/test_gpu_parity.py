@@ -296,3 +296,28 @@ def test_tensor_core_edge_shapes(n, d, b, m):
         got = sap.col_dist_matmul(o, W, B)
         ref = orc.col_dist_matmul(orc.Points(fam, ls, 0.9, X), W, B, workers=8)
         assert rel(got, ref) < TOL_BLOCK, (fam, rel(got, ref))
+
+
+def test_long_trajectory_full_lookahead_batches():
+    """80 iterations: the lookahead ramps 1, 2, 4, 8, 16 to full 32-iteration
+    batches (batched gathers, K_BB tiles and power iterations, stepsizes
+    copied to the trace once per batch, 1/rho folded into the update's
+    stepsize); blocks, stepsizes and the iterate against the oracle."""
+    rng = np.random.default_rng(31)
+    n, d, b, r, m, iters = 4000, 5, 512, 40, 3, 80
+    X = rng.uniform(-2.0, 2.0, size=(n, d))
+    Y = rng.standard_normal((n, m))
+    ls = np.full(d, 1.1)
+    lam = 1e-2
+    pts = orc.Points("matern32", ls, 1.0, X)
+    W_ref, eta_ref, crc_ref, _ = orc.adasap_solve(pts, lam, Y, iters, 3, b, r, workers=8)
+    o = sap.KernelOracle(sap.KernelSpec("matern32", ls, 1.0), X, lam)
+    cfg = sap.RunConfig(lam=lam, blocksize=b, nystrom_rank=r, residual_every=0, seed=3,
+                        max_iters=iters)
+    assert cfg.lookahead == 32
+    res = sap.adasap_solve(o, Y, cfg)
+    crcs = np.array([rec.block_hash for rec in res.trace.records])
+    assert np.array_equal(crcs, crc_ref)
+    etas = np.array([rec.stepsize for rec in res.trace.records])
+    assert np.abs(etas - eta_ref).max() / np.abs(eta_ref).max() < 1e-4
+    assert rel(res.W, W_ref) < 2e-3
