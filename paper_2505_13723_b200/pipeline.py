@@ -28,7 +28,6 @@ allocated in steady state.
 
 from __future__ import annotations
 
-import math
 import os
 import sys
 import time
@@ -355,7 +354,7 @@ class Lookahead:
     def _produce(self, slot, t0, count, side, owner=0):
         if owner != self.shard.rank:
             return self._produce_blocks(slot, t0, count, side, owner)
-        b, r, seed, n = self.b, self.r, self.seed, self.n
+        b, r = self.b, self.r
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
         tm0 = time.perf_counter()

@@ -43,10 +43,9 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .dist import WorkerPool
 from .errors import ConfigError, ContractError
 from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
-from .parallel import ShardInfo, allreduce_sum_, current_shard, gather_rows
+from .parallel import allreduce_sum_, current_shard, gather_rows
 from .pipeline import Lookahead
 from .rng import block_hash
 
