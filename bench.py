@@ -52,8 +52,8 @@ METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=40)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--family", default=CONFIG["family"])
     ap.add_argument("--n", type=int, default=CONFIG["n"])
