@@ -247,13 +247,15 @@ __global__ void colabsmax_kernel(const float *A, int64_t lda, int64_t n, float *
 
 __global__ void tc_reduce_kernel(const float *part, int splits, int64_t b, int m, float variance,
                                  const float *zscale, float *out, int64_t ldo, int accumulate) {
+  // partials are [splits][m][b] (block rows contiguous): consecutive threads
+  // take consecutive rows of one column, so every partial load is coalesced
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= b * m) return;
-  const int64_t i = e / m;
-  const int c = int(e % m);
+  const int c = int(e / b);
+  const int64_t i = e % b;
   // eight independent partial sums: eight loads in flight per thread (the
   // partials of one element are b*m floats apart; a single running sum left
-  // the kernel latency-bound at ~1.8 TB/s)
+  // the kernel latency-bound)
   const int64_t bm = b * m;
   const float *pe = part + e;
   float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};

@@ -93,7 +93,7 @@ struct Params {
   int row_tiles;
   int splits;
   int64_t tiles;           // column tiles of NT points
-  float *part;             // [splits][b][m] partial sums (scaled)
+  float *part;             // [splits][m][b] partial sums (scaled; rows contiguous)
   int debug;               // profiling switches, 0 in production
   unsigned long long *prof;  // per-CTA role timers (SAP_TC_DEBUG=9), else NULL
 };
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pend_live) {
 #pragma unroll
           for (int c = 0; c < NACC; ++c)
-            if (g0 + c < g1 && g0 + c < p.m) pend_dst[g0 + c] = acc[c];
+            if (g0 + c < g1 && g0 + c < p.m) pend_dst[int64_t(g0 + c) * p.b] = acc[c];
         }
 #pragma unroll
         for (int c = 0; c < NACC; ++c) acc[c] = 0.0f;
@@ -434,10 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       split_range(p.tiles, p.splits, split, t0, t1);
       const int64_t grow = int64_t(rt) * BM + row_in_tile;
       const bool live = grow < p.b;
-      float *dst = p.part + (int64_t(split) * p.b + (live ? grow : 0)) * p.m;
+      float *dst = p.part + int64_t(split) * p.m * p.b + (live ? grow : 0);
       const int64_t rid = (p.row_ids && live) ? p.row_ids[grow] : INT64_MIN;
       if (t1 == t0 && live)
-        for (int c = g0; c < g1 && c < p.m; ++c) dst[c] = 0.0f;
+        for (int c = g0; c < g1 && c < p.m; ++c) dst[int64_t(c) * p.b] = 0.0f;
       int seg_j = 0;
       for (int64_t t = t0; t < t1; ++t) {
         tc::mbar_wait(sfull0 + 8 * r, ph);

@@ -368,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int c = (w + k * kEpiGroups) * 8 + e;
-              if (k < ngran && c < p.m) pend_dst[c] = acc[k * 8 + e];
+              if (k < ngran && c < p.m) pend_dst[int64_t(c) * p.b] = acc[k * 8 + e];
             }
         }
 #pragma unroll
@@ -381,13 +381,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       split_range(p.tiles, p.splits, split, t0, t1);
       const int64_t grow = int64_t(rt) * 2 * BM + int64_t(cr) * BM + row_in_tile;
       const bool live = grow < p.b;
-      float *dst = p.part + (int64_t(split) * p.b + (live ? grow : 0)) * p.m;
+      float *dst = p.part + int64_t(split) * p.m * p.b + (live ? grow : 0);
       const int64_t rid = (p.row_ids && live) ? p.row_ids[grow] : INT64_MIN;
       if (t1 == t0 && live) {
         for (int k = 0; k < ngran; ++k)
           for (int e = 0; e < 8; ++e) {
             const int c = (w + k * kEpiGroups) * 8 + e;
-            if (c < p.m) dst[c] = 0.0f;
+            if (c < p.m) dst[int64_t(c) * p.b] = 0.0f;
           }
       }
       int seg_j = 0;
