@@ -22,6 +22,8 @@
  *   sap_ktile(64)       <- KernelOracle.tile / .block / .dense   kernels.py:118-143
  *   sap_grad_gather     <- grad = K[B,:]Z + lam Z[B] - Y[B]     solvers.py:376-377
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
+ *   sap_woodbury_apply  <- apply_inv (Nystrom-Woodbury)         randnla.py:109-134
+ *   sap_block_step      <- Phases I(tail)-IV of adasap_step     solvers.py:376-401
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
  *   sap_sdd_update      <- sdd_solve's momentum/averaging step  solvers.py:487-493
@@ -282,6 +284,106 @@ int *sap_normal_status(void *ws);
  */
 int sap_host_draws(uint64_t seed, int64_t t0, int count, int64_t n, int64_t b, int64_t *blocks,
                    uint32_t *crcs, int64_t *omega_states, double *v0, int nthreads);
+
+/* ---- Phase IV in one launch (phase4.cu) -------------------------------- */
+
+/*
+ * Arguments of sap_block_step: one ADASAP iteration after the block-row
+ * product (solvers.py:376-401). All arrays are device memory.
+ */
+typedef struct sap_step_args {
+  /* gradient source: the tensor-core partials [splits][m][b] left in the
+   * sap_krows_tc_next workspace (reduce = 0; scaled by 2^14 zscale[c]), or,
+   * with part == NULL, a reduced product G (b x m fp32, row-major, ldg) */
+  const float *part;
+  int splits;
+  float variance;
+  const float *zscale;
+  const float *G;
+  int64_t ldg;
+  /* lam Z[B] - Y[B] with Z = zp*P + zq*Q (column-major m x ldp, Q nullable) */
+  const float *P, *Q, *Y;
+  int64_t ldp;
+  double zp, zq, lam;
+  const int64_t *loc; /* block row i -> local row, or -1 (owned by another rank) */
+  int64_t b;
+  int m;
+  double *g;          /* gradient, b x m fp64 row-major (ldgo): out (GRAD) / in (APPLY only) */
+  int64_t ldgo;
+  /* Woodbury: D = g - UMc (U^T g), U and UMc = U Mc b x r fp64 row-major (ldu);
+   * Mc = (rho S^-1 + U^T U)^-1 (randnla.py:109-134); r = 0: D = g */
+  const double *U, *UMc;
+  int64_t ldu;
+  int r;
+  /* lazy Nesterov update of the owned block rows (sap_pq_update semantics;
+   * eta_dev[0] is eta/rho); Pw == NULL skips the update */
+  float *Pw, *Qw;
+  const double *eta_dev;
+  double e0, e1;
+  float *WB;
+  int64_t ldwb;
+  float *Pb, *Qb;
+  /* optional D output, D * (1 / dscale_dev[0]) (dscale_dev nullable) */
+  double *D;
+  int64_t ldd;
+  const double *dscale_dev;
+  /* optional next tensor-core operand (the buffer sap_krows_tc_next filled):
+   * the updated block rows' Z_{t+1} = zp1*P + zq1*Q are written into it; if
+   * one leaves its column's scale, the whole buffer is rebuilt in the same
+   * launch. zflag: two device ints, zero-initialised; flag_idx alternates
+   * 0/1 per call */
+  void *Zhi_next, *Zlo_next;
+  int64_t ldz;
+  float *zscale_next;
+  double zp1, zq1;
+  int *zflag;
+  int flag_idx;
+  int64_t n_local;
+} sap_step_args;
+
+enum { SAP_STEP_GRAD = 1, SAP_STEP_APPLY = 2 };
+
+/* Workspace bytes of sap_block_step / sap_woodbury_apply; the first 256
+ * bytes (grid barrier) must be zeroed once before the first call. */
+size_t sap_block_step_workspace(int64_t b, int r, int m);
+
+/*
+ * mode GRAD: g = K[B,:]Z + lam Z[B] - Y[B] (solvers.py:376-377) -- the
+ *   per-rank part before the all-reduce of g;
+ * mode APPLY: D = g - UMc U^T g, then the update / D output / next operand;
+ * GRAD|APPLY: both in one cooperative launch (one GPU).
+ * Replaces sap_grad_gather + apply_inv (randnla.py:109-134) + sap_pq_update.
+ */
+int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_bytes,
+                   void *stream);
+
+/*
+ * D = (g - UMc (U^T g)) / rho_dev[0]: the Nystrom-preconditioned block
+ * direction of apply_inv (randnla.py:109-134) for b x m fp64 g, with
+ * UMc = U (rho S^-1 + U^T U)^-1 precomputed (the Cholesky solve of the
+ * reference folded into the r x r core). Workspace: sap_block_step_workspace.
+ */
+int sap_woodbury_apply(const double *U, const double *UMc, int64_t ldu, int64_t b, int r,
+                       const double *g, int64_t ldg, int m, const double *rho_dev, double *D,
+                       int64_t ldd, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * sap_krows_tc plus two options for the solver:
+ *  - reduce = 0 leaves the unreduced partials in ws ([splits][m][b], for
+ *    sap_block_step) and stores the split count in *splits_out;
+ *  - Zhi_next != NULL also fills the NEXT iterate's operand
+ *    Z_{t+1} = zp*P + zq*Q (scale from the bounds Pb/Qb) into Zhi_next /
+ *    Zlo_next / zscale_next: inside the block-row kernel by its otherwise idle
+ *    control warps (the CTA-pair kernel), else by a separate sap_z_operand pass.
+ */
+int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
+                      const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
+                      const void *Zlo, int nz, int64_t ldz, const float *zscale, int m,
+                      int family, double variance, float *out, int64_t ldo, int accumulate,
+                      void *ws, size_t ws_bytes, int reduce, int *splits_out, const float *P,
+                      const float *Q, int64_t ldp, double zp, double zq, const float *Pb,
+                      const float *Qb, void *Zhi_next, void *Zlo_next, float *zscale_next,
+                      void *stream);
 
 #ifdef __cplusplus
 }

@@ -68,7 +68,32 @@ SIGNATURES = {
     "sap_host_draws": (_I, [ctypes.c_uint64, _I64, _I, _I64, _I64, _P, _P, _P, _P, _I]),
     "sap_krows_tc": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I64, _P, _P, _I, _I64, _P, _I, _I, _D,
                           _P, _I64, _I, _P, _SZ, _P]),
+    "sap_krows_tc_next": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I64, _P, _P, _I, _I64, _P, _I,
+                               _I, _D, _P, _I64, _I, _P, _SZ, _I, _P, _P, _P, _I64, _D, _D, _P,
+                               _P, _P, _P, _P, _P]),
+    "sap_block_step_workspace": (_SZ, [_I64, _I, _I]),
+    "sap_block_step": (_I, [_P, _I, _P, _SZ, _P]),
+    "sap_woodbury_apply": (_I, [_P, _P, _I64, _I64, _I, _P, _I64, _I, _P, _P, _I64, _P, _SZ, _P]),
 }
+
+
+class StepArgs(ctypes.Structure):
+    """``sap_step_args`` (include/sapgp_b200.h): arguments of sap_block_step."""
+    _fields_ = [
+        ("part", _P), ("splits", _I), ("variance", ctypes.c_float), ("zscale", _P),
+        ("G", _P), ("ldg", _I64),
+        ("P", _P), ("Q", _P), ("Y", _P), ("ldp", _I64), ("zp", _D), ("zq", _D), ("lam", _D),
+        ("loc", _P), ("b", _I64), ("m", _I), ("g", _P), ("ldgo", _I64),
+        ("U", _P), ("UMc", _P), ("ldu", _I64), ("r", _I),
+        ("Pw", _P), ("Qw", _P), ("eta_dev", _P), ("e0", _D), ("e1", _D), ("WB", _P),
+        ("ldwb", _I64), ("Pb", _P), ("Qb", _P),
+        ("D", _P), ("ldd", _I64), ("dscale_dev", _P),
+        ("Zhi_next", _P), ("Zlo_next", _P), ("ldz", _I64), ("zscale_next", _P), ("zp1", _D),
+        ("zq1", _D), ("zflag", _P), ("flag_idx", _I), ("n_local", _I64),
+    ]
+
+
+STEP_GRAD, STEP_APPLY = 1, 2
 
 _lib = None
 

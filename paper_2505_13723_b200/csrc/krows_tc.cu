@@ -158,29 +158,16 @@ __global__ void gather_cols_kernel(const float *RA, int ka, int d, int rbf, cons
   out[e] = v;
 }
 
-// Z operand: ZT_hi/ZT_lo[c][j] = fp16 split of scale_c * (zp P[c][j] + zq Q[c][j]),
-// scale_c = 2^floor(log2(16384 / bound_c)) from per-column magnitude bounds.
-// Rows c >= m (MMA padding) are not touched: the caller zeroes them once.
-__device__ __forceinline__ float z_scale(float zp, float zq, const float *Pb, const float *Qb,
-                                         bool hasq, int c) {
-  const float bound = fabsf(zp) * Pb[c] + (hasq ? fabsf(zq) * Qb[c] : 0.0f);
-  float sc = 1.0f;
-  if (bound > 0.0f && isfinite(bound)) sc = exp2f(floorf(log2f(16384.0f / bound)));
-  return fminf(fmaxf(sc, 0x1p-100f), 0x1p100f);
-}
-
-__device__ __forceinline__ void z_split(float z, __half &h, __half &l) {
-  h = __float2half_rn(z);
-  l = __float2half_rn(z - __half2float(h));
-}
-
+// The operand passes use the shared helpers of zop.cuh, so the stand-alone
+// pass, the block-row kernel's overlapped pass and the Phase IV patch write
+// bit-identical operands.
 // vectorised form: 8 consecutive points per thread (2 x float4 from P and Q,
 // one 16-byte store each to Zhi and Zlo); needs 16-byte aligned rows
 __global__ void z_operand_vec_kernel(const float *P, const float *Q, int64_t ldp, int64_t n,
                                      float zp, float zq, const float *Pb, const float *Qb,
                                      int64_t ldz, __half *Zhi, __half *Zlo, float *zscale) {
   const int c = blockIdx.y;
-  const float sc = z_scale(zp, zq, Pb, Qb, Q != nullptr, c);
+  const float sc = zop::scale(zp, zq, Pb, Qb, Q != nullptr, c);
   if (blockIdx.x == 0 && threadIdx.x == 0) zscale[c] = sc;
   const float a = zp * sc, bq = zq * sc;
   const float *pr = P + int64_t(c) * ldp;
@@ -188,31 +175,8 @@ __global__ void z_operand_vec_kernel(const float *P, const float *Q, int64_t ldp
   for (int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; j < ldz;
        j += int64_t(gridDim.x) * blockDim.x * 8) {
     float z[8];
-    if (j + 8 <= n) {
-      const float4 p0 = *reinterpret_cast<const float4 *>(pr + j);
-      const float4 p1 = *reinterpret_cast<const float4 *>(pr + j + 4);
-      z[0] = a * p0.x; z[1] = a * p0.y; z[2] = a * p0.z; z[3] = a * p0.w;
-      z[4] = a * p1.x; z[5] = a * p1.y; z[6] = a * p1.z; z[7] = a * p1.w;
-      if (qr) {
-        const float4 q0 = *reinterpret_cast<const float4 *>(qr + j);
-        const float4 q1 = *reinterpret_cast<const float4 *>(qr + j + 4);
-        z[0] = fmaf(bq, q0.x, z[0]); z[1] = fmaf(bq, q0.y, z[1]);
-        z[2] = fmaf(bq, q0.z, z[2]); z[3] = fmaf(bq, q0.w, z[3]);
-        z[4] = fmaf(bq, q1.x, z[4]); z[5] = fmaf(bq, q1.y, z[5]);
-        z[6] = fmaf(bq, q1.z, z[6]); z[7] = fmaf(bq, q1.w, z[7]);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int64_t jj = j + e;
-        z[e] = jj < n ? (qr ? fmaf(bq, qr[jj], a * pr[jj]) : a * pr[jj]) : 0.0f;
-      }
-    }
-    __align__(16) __half h[8], l[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) z_split(z[e], h[e], l[e]);
-    *reinterpret_cast<uint4 *>(Zhi + int64_t(c) * ldz + j) = *reinterpret_cast<const uint4 *>(h);
-    *reinterpret_cast<uint4 *>(Zlo + int64_t(c) * ldz + j) = *reinterpret_cast<const uint4 *>(l);
+    zop::load8<false>(pr, qr, j, n, a, bq, z);
+    zop::store8<false>(z, Zhi + int64_t(c) * ldz, Zlo + int64_t(c) * ldz, j);
   }
 }
 
@@ -220,7 +184,7 @@ __global__ void z_operand_kernel(const float *P, const float *Q, int64_t ldp, in
                                  float zp, float zq, const float *Pb, const float *Qb,
                                  int64_t ldz, __half *Zhi, __half *Zlo, float *zscale) {
   const int c = blockIdx.y;
-  const float sc = z_scale(zp, zq, Pb, Qb, Q != nullptr, c);
+  const float sc = zop::scale(zp, zq, Pb, Qb, Q != nullptr, c);
   if (blockIdx.x == 0 && threadIdx.x == 0) zscale[c] = sc;
   for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < ldz;
        j += int64_t(gridDim.x) * blockDim.x) {
@@ -230,7 +194,7 @@ __global__ void z_operand_kernel(const float *P, const float *Q, int64_t ldp, in
       if (Q) z = fmaf(zq, Q[int64_t(c) * ldp + j], z);
       z *= sc;
     }
-    z_split(z, Zhi[int64_t(c) * ldz + j], Zlo[int64_t(c) * ldz + j]);
+    zop::split(z, Zhi[int64_t(c) * ldz + j], Zlo[int64_t(c) * ldz + j]);
   }
 }
 
@@ -443,17 +407,23 @@ size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols) {
   return size_t(s) * size_t(b) * size_t(m) * sizeof(float);
 }
 
-int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
-                 const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
-                 const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
-                 double variance, float *out, int64_t ldo, int accumulate, void *ws,
-                 size_t ws_bytes, void *stream) {
+int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
+                      const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
+                      const void *Zlo, int nz, int64_t ldz, const float *zscale, int m,
+                      int family, double variance, float *out, int64_t ldo, int accumulate,
+                      void *ws, size_t ws_bytes, int reduce, int *splits_out, const float *P,
+                      const float *Q, int64_t ldp, double zp, double zq, const float *Pb,
+                      const float *Qb, void *Zhi_next, void *Zlo_next, float *zscale_next,
+                      void *stream) {
   const bool half = ka == tck2::kKaF16;  // 32 fp16 features per point
   if (b <= 0 || m <= 0 || ncols <= 0 || (ka != 32 && ka != 64 && !half) || nz % 16 || nz < m ||
       nz > 128 || bpad % BM || bpad < b || ldz % 8 || ldz < ncols || ncols > INT32_MAX)
     return fail(SAP_ERR_CONTRACT, "krows_tc: bad shape b=%lld m=%d nz=%d ncols=%lld ka=%d",
                 (long long)b, m, nz, (long long)ncols, ka);
-  if (ldo < m) return fail(SAP_ERR_CONTRACT, "krows_tc: ldo < m");
+  if (reduce && ldo < m) return fail(SAP_ERR_CONTRACT, "krows_tc: ldo < m");
+  if (!reduce && !splits_out) return fail(SAP_ERR_CONTRACT, "krows_tc: splits_out is NULL");
+  if (Zhi_next && (!Zlo_next || !zscale_next || !P || !Pb || (Q && !Qb)))
+    return fail(SAP_ERR_CONTRACT, "krows_tc: next operand arguments incomplete");
   const bool pair = use_pair(nz, ka) && bpad % (2 * BM) == 0;
   if (half && !pair)
     return fail(SAP_ERR_CONTRACT, "krows_tc: fp16 features need the CTA-pair kernel "
@@ -484,6 +454,15 @@ int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t
   if (!ws || ws_bytes < need)
     return fail(SAP_ERR_CONTRACT, "krows_tc: workspace %zu < %zu bytes", ws_bytes, need);
   p.part = static_cast<float *>(ws);
+  // the next operand inside the CTA-pair kernel (16-byte vector rows only)
+  auto al16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const bool side = Zhi_next && pair && ldp % 4 == 0 && ldz % 8 == 0 && al16(P) &&
+                    (!Q || al16(Q)) && al16(Zhi_next) && al16(Zlo_next) &&
+                    getenv("SAP_ZNEXT_SEPARATE") == nullptr;
+  if (side)
+    p.zn = zop::Next{P, Q, ldp, ncols, m, float(zp), float(zq), Pb, Qb,
+                     static_cast<__half *>(Zhi_next), static_cast<__half *>(Zlo_next), ldz,
+                     zscale_next};
   if (!pair && !tc_fits(nz, ka))
     return fail(SAP_ERR_CONTRACT, "krows_tc: nz=%d ka=%d tile ring does not fit shared memory", nz,
                 ka);
@@ -544,11 +523,30 @@ int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t
               n0 ? s0 / n0 : 0.0, n1 ? s1 / n1 : 0.0);
     }
   }
+  if (Zhi_next && !side &&
+      (rc = sap_z_operand(P, Q, ldp, ncols, m, zp, zq, Pb, Qb, nz, ldz, Zhi_next, Zlo_next,
+                          zscale_next, stream)) != SAP_OK)
+    return rc;
+  if (!reduce) {
+    *splits_out = p.splits;
+    return SAP_OK;
+  }
   const int64_t tot = b * m;
   tc_reduce_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(p.part, p.splits, b, m,
                                                                 float(variance), zscale, out, ldo,
                                                                 accumulate);
   return check_launch("tc_reduce_kernel");
+}
+
+int sap_krows_tc(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
+                 const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
+                 const void *Zlo, int nz, int64_t ldz, const float *zscale, int m, int family,
+                 double variance, float *out, int64_t ldo, int accumulate, void *ws,
+                 size_t ws_bytes, void *stream) {
+  return sap_krows_tc_next(CA, ncols, ka, RAg, bpad, row_ids, b, col_base, Zhi, Zlo, nz, ldz,
+                           zscale, m, family, variance, out, ldo, accumulate, ws, ws_bytes, 1,
+                           nullptr, nullptr, nullptr, 0, 0.0, 0.0, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, stream);
 }
 
 }  // extern "C"

@@ -39,6 +39,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "zop.cuh"
 
 namespace sap {
 namespace tck {
@@ -96,6 +97,7 @@ struct Params {
   float *part;             // [splits][m][b] partial sums (scaled; rows contiguous)
   int debug;               // profiling switches, 0 in production
   unsigned long long *prof;  // per-CTA role timers (SAP_TC_DEBUG=9), else NULL
+  zop::Next zn;            // next iterate's operand (CTA-pair kernel side job; Zhi NULL: none)
 };
 
 template <int NZ, int KA>

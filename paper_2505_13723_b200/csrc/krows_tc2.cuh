@@ -70,7 +70,7 @@ constexpr int kThreads = 128 * (1 + kEpiGroups);    // + the control warpgroup
 // increases can only draw what the control warpgroup's decrease released,
 // otherwise setmaxnreg.inc spins forever
 constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;
-constexpr int kCtlRegs = 40;
+constexpr int kCtlRegs = 64;  // warps 2-3 stream the next operand (zop::next_pass)
 constexpr int kEpiRegs = 104;
 static_assert(128 * kCtlRegs + 128 * kEpiGroups * kEpiRegs <= kThreads * kLaunchRegs,
               "setmaxnreg budget exceeds the launch allocation");
@@ -318,7 +318,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         p.prof[blockIdx.x * 16 + 6] = i2;
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    // ============ next iterate's operand (warps 2-3, otherwise idle) ============
+    // Z_{t+1} = zp P + zq Q into the second operand buffer while this kernel
+    // consumes Z_t: ~5 MB per CTA streamed over the kernel's lifetime (HBM is
+    // <10% busy here), instead of a separate HBM-bound pass on the critical
+    // path between two block-row products. The block rows are patched by
+    // the Phase IV kernel after the update (phase4.cu).
+    if (p.zn.Zhi) zop::next_pass(p.zn, blockIdx.x, gridDim.x, (warp - 2) * 32 + lane, 64);
+  } else {
     // ===================== epilogue (both CTAs) =====================
     // Four warpgroups, i.e. four warps per SM sub-partition, so TMEM load/store
     // and dependency latencies hide behind the other warps' MUFU/FMA work:

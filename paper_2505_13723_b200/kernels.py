@@ -21,6 +21,7 @@ tensors.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from dataclasses import dataclass
@@ -274,6 +275,31 @@ def krows_tc(spec, tcp, RAg, b, row_ids, zop, out, ws=None, accumulate=False, co
              nat.ptr(zop.scale), zop.m, spec.code, spec.variance, nat.ptr(out), out.stride(0),
              int(accumulate), nat.ptr(ws), ws.numel() * 4, nat.stream_handle())
     return out
+
+
+def krows_tc_partials(spec, tcp, RAg, b, row_ids, zop, ws, nxt=None):
+    """The block-row product's unreduced partials ([splits][m][b] in ``ws``,
+    reduced by the fused Phase IV kernel, sap_block_step) and, with
+    ``nxt = (P, Q, zp, zq, Pb, Qb, zop_next)``, the next iterate's operand
+    Z_{t+1} = zp P + zq Q filled into ``zop_next`` inside the same kernel.
+    Returns the split count."""
+    CA, col_base, ncols = tcp.CA, tcp.lo, tcp.hi - tcp.lo
+    need = nat.load().sap_krows_tc_workspace(b, zop.m, ncols)
+    if ws.numel() * ws.element_size() < need:
+        raise ContractError("block-row workspace too small")
+    if nxt is not None:
+        P, Q, zp, zq, Pb, Qb, zn = nxt
+        extra = (nat.ptr(P), nat.ptr(Q), P.stride(0), zp, zq, nat.ptr(Pb), nat.ptr(Qb),
+                 nat.ptr(zn.hi), nat.ptr(zn.lo), nat.ptr(zn.scale))
+    else:
+        extra = (None, None, 0, 0.0, 0.0, None, None, None, None, None)
+    splits = ctypes.c_int(0)
+    nat.call("sap_krows_tc_next", nat.ptr(CA), ncols, tcp.ka_code, nat.ptr(RAg), RAg.shape[0],
+             nat.ptr(row_ids), b, col_base, nat.ptr(zop.hi), nat.ptr(zop.lo), zop.nz, zop.ldz,
+             nat.ptr(zop.scale), zop.m, spec.code, spec.variance, None, zop.m, 0, nat.ptr(ws),
+             ws.numel() * ws.element_size(), 0, ctypes.byref(splits), *extra,
+             nat.stream_handle())
+    return splits.value
 
 
 def ktile_f32(spec, A, asq, aid, C, csq, cid, ldx, d, out):

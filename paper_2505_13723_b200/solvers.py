@@ -34,7 +34,9 @@ contains the failing iteration.
 
 from __future__ import annotations
 
+import ctypes
 import math
+import os
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -44,7 +46,7 @@ import torch
 
 from . import _native as nat
 from .errors import ConfigError, ContractError
-from .kernels import KernelOracle, ZOperand, krows_tc, krows_times, to_colmajor
+from .kernels import KernelOracle, ZOperand, krows_tc, krows_tc_partials, krows_times, to_colmajor
 from .parallel import allreduce_sum_, current_shard, gather_rows
 from .pipeline import Lookahead
 from .rng import block_hash
@@ -348,6 +350,24 @@ class AdasapEngine:
             self.tcp = self.zop = self.Pb = self.Qb = None
             need = nat.load().sap_krows_workspace(b, m, max(nl, 1))
         self.ws = torch.empty(max(need // 4 + 1, 1), dtype=f32, device=self.dev)
+        # Phase IV in one launch (sap_block_step, csrc/phase4.cu): gradient
+        # gather + Woodbury apply + lazy update + the next operand's block rows;
+        # SAP_FUSED_STEP=0 selects the unfused chain (grad_gather, two GEMMs,
+        # pq_update, separate operand pass) for A/B runs
+        self.fused = os.environ.get("SAP_FUSED_STEP", "1") == "1" and not self.dense
+        lib = nat.load()
+        self.p4ws = torch.zeros(lib.sap_block_step_workspace(b, self.r, m) // 8 + 1,
+                                dtype=torch.float64, device=self.dev)
+        self.zflag = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        self._fi = 0
+        # the next iterate's operand buffer, filled inside the block-row kernel
+        # (double buffering; skipped when the state would not fit beside it)
+        self.zop_next = None
+        if self.fused and self.use_tc:
+            free, _ = torch.cuda.mem_get_info(self.dev)
+            if free > 2 * self.zop.hi.numel() * 2 + (4 << 30):
+                self.zop_next = ZOperand(m, nl, self.dev)
+        self.z_stale = True  # zop does not hold Z_t yet (filled by the first step)
         self.t = 0
         self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
                             config.lookahead, identity_precond, tcp=self.tcp)
@@ -359,6 +379,9 @@ class AdasapEngine:
     # -- one iteration ------------------------------------------------------------
     def step(self, point=None):
         """One ADASAP iteration; returns the host IterPlan (block, crc, rho)."""
+        if point is None and self.fused:
+            return self._step_fused()
+        self.z_stale = True
         plan = self.la.get(self.t)
         sh = self.shard
         zp, zq = self._u1y, self.s * self._u2y
@@ -401,6 +424,92 @@ class AdasapEngine:
         self.t += 1
         return plan
 
+    def _step_fused(self):
+        """Phase I on the block-row kernel (partials left unreduced; the next
+        iterate's operand streamed by the same kernel), then Phases I(tail)-IV
+        in one cooperative launch (sap_block_step): gradient gather, all-reduce
+        (several ranks: between a GRAD and an APPLY launch), Woodbury apply
+        D = g - U Mc U^T g (randnla.py:109-134), lazy Nesterov update of the
+        block rows (solvers.py:76-85) and Z_{t+1} at those rows."""
+        plan = self.la.get(self.t)
+        sh, lib = self.shard, nat.load()
+        zp, zq = self._u1y, self.s * self._u2y
+        e0, e1, s_next = self._coeffs()
+        zq1 = s_next * self._u2y
+        a = nat.StepArgs()
+        zn = self.zop_next
+        if sh.size > 0 and self.use_tc:
+            if self.z_stale:
+                self.zop.fill(self.P, self.Q, zp, zq, self.Pb, self.Qb)
+            nxt = (self.P, self.Q, zp, zq1, self.Pb, self.Qb, zn) if zn is not None else None
+            a.splits = krows_tc_partials(self.o.spec, self.tcp, plan.RAg, self.b, plan.block_dev,
+                                         self.zop, self.ws, nxt)
+            a.part, a.variance, a.zscale = nat.ptr(self.ws), self.o.spec.variance, \
+                nat.ptr(self.zop.scale)
+        else:
+            if sh.size > 0:
+                krows_times(self.o.spec, self.o.points, plan.Xb, plan.rsq, plan.block_dev,
+                            self.P, self.G, col_base=sh.lo, R2=self.Q, ca=zp, cb=zq, ws=self.ws,
+                            ncols=sh.size, col_offset=sh.lo)
+            else:
+                self.G.zero_()
+            a.G, a.ldg = nat.ptr(self.G), self.G.stride(0)
+        a.P, a.Q, a.Y, a.ldp = nat.ptr(self.P), nat.ptr(self.Q), nat.ptr(self.Y), self.ld
+        a.zp, a.zq, a.lam = zp, zq, self.lam
+        a.loc, a.b, a.m = nat.ptr(plan.loc_dev), self.b, self.m
+        a.g, a.ldgo = nat.ptr(self.g), self.g.stride(0)
+        if plan.U is not None:
+            a.U, a.UMc, a.ldu, a.r = nat.ptr(plan.U), nat.ptr(plan.UMc), plan.U.stride(0), self.r
+        a.Pw, a.Qw, a.eta_dev, a.e0, a.e1 = nat.ptr(self.P), nat.ptr(self.Q), \
+            nat.ptr(plan.eta_rho_dev), e0, e1
+        a.WB, a.ldwb, a.Pb, a.Qb = nat.ptr(self.WB), self.WB.stride(0), nat.ptr(self.Pb), \
+            nat.ptr(self.Qb)
+        if zn is not None and sh.size > 0:
+            a.Zhi_next, a.Zlo_next, a.ldz, a.zscale_next = nat.ptr(zn.hi), nat.ptr(zn.lo), \
+                zn.ldz, nat.ptr(zn.scale)
+            a.zp1, a.zq1, a.zflag, a.flag_idx = zp, zq1, nat.ptr(self.zflag), self._fi
+            a.n_local = sh.size
+            self._fi ^= 1
+        ws, wsb, st = nat.ptr(self.p4ws), self.p4ws.numel() * 8, nat.stream_handle()
+        if sh.world == 1:
+            nat.check(lib.sap_block_step(ctypes.byref(a), nat.STEP_GRAD | nat.STEP_APPLY, ws, wsb,
+                                         st))
+        else:
+            nat.check(lib.sap_block_step(ctypes.byref(a), nat.STEP_GRAD, ws, wsb, st))
+            allreduce_sum_(self.g)
+            nat.check(lib.sap_block_step(ctypes.byref(a), nat.STEP_APPLY, ws, wsb, st))
+        if zn is not None and sh.size > 0:
+            self.zop, self.zop_next = zn, self.zop
+            self.z_stale = False
+        else:
+            self.z_stale = True
+        self._advance(s_next)
+        if self.t == plan.batch_t0:  # the batch's stepsizes into the trace, once per batch
+            self.etas[self.t:self.t + plan.batch_eta.numel()].copy_(plan.batch_eta)
+        self.last_loc = plan.loc_dev
+        self.crcs.append(plan.crc)
+        self.t += 1
+        return plan
+
+    def _coeffs(self):
+        """(e0, e1, s_next): the block rows' update of [P; Q] in the next basis,
+        e = M_{t+1}^{-1} (-gamma, -(1 - alpha)) (2 x 2 closed form)."""
+        delta = (-self.gamma, -(1.0 - self.alpha))
+        s_next = self.lam2 * self.s
+        a, c = self._u1x, self._u1y
+        bb, dd = s_next * self._u2x, s_next * self._u2y
+        det = a * dd - bb * c
+        return (delta[0] * dd - bb * delta[1]) / det, (a * delta[1] - c * delta[0]) / det, s_next
+
+    def _advance(self, s_next):
+        self.s_prev, self.s = self.s, s_next
+        if abs(s_next) < RENORM_LO or abs(s_next) > RENORM_HI:
+            self.Q.mul_(s_next)
+            if self.Qb is not None:
+                self.Qb.mul_(abs(s_next))
+            self.s_prev /= s_next
+            self.s = 1.0
+
     @property
     def M(self):
         return np.column_stack([self.u1, self.s * self.u2])
@@ -422,21 +531,9 @@ class AdasapEngine:
             self.Q.mul_(1.0 - alpha).add_(P, alpha=alpha)
             self._pq(plan, D, M, delta[0], delta[1], wb=False)
             return
-        s_next = self.lam2 * self.s
-        # e = M_next^{-1} delta, M_next = [[a, s b], [c, s d]] (2x2 closed form)
-        a, c = self._u1x, self._u1y
-        bb, dd = s_next * self._u2x, s_next * self._u2y
-        det = a * dd - bb * c
-        e0 = (delta[0] * dd - bb * delta[1]) / det
-        e1 = (a * delta[1] - c * delta[0]) / det
+        e0, e1, s_next = self._coeffs()
         self._pq(plan, D, M, e0, e1)
-        self.s_prev, self.s = self.s, s_next
-        if abs(s_next) < RENORM_LO or abs(s_next) > RENORM_HI:
-            self.Q.mul_(s_next)
-            if self.Qb is not None:
-                self.Qb.mul_(abs(s_next))
-            self.s_prev /= s_next
-            self.s = 1.0
+        self._advance(s_next)
 
     def _pq(self, plan, D, M, e0, e1, wb=True):
         nat.call("sap_pq_update", nat.ptr(self.P), nat.ptr(self.Q), self.ld,
