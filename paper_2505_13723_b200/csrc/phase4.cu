@@ -1,5 +1,5 @@
-// Phase IV of an ADASAP iteration (solvers.py:376-401) in four stream-ordered
-// launches of one kernel: the gradient gather, the Nystrom-Woodbury apply and
+// Phase IV of an ADASAP iteration (solvers.py:376-401) in three stream-ordered
+// launches: the gradient gather, the Nystrom-Woodbury apply and
 // the lazy Nesterov block update, plus the block rows of the next iterate's
 // tensor-core operand.
 //
@@ -13,8 +13,8 @@
 //                                                   on the stepsize eta/rho)
 //      lazy update of the block rows (sap_pq_update's arithmetic),
 //      Z_{t+1}[B] into the next operand buffer, overflow flag
-//   -- launch (only with a next operand) --
-//   E  if an updated block row left the next operand's scale: rebuild it
+//   E  if an updated block row left the next operand's scale: the last CTA of
+//      D rebuilds it (rare: the scale leaves 64x headroom)
 //
 // The two small fp64 GEMMs (B: r x m x rows, D: rows x m x r per CTA) run on
 // the FP64 tensor cores (mma.sync m8n8k4 .f64) from shared-memory tiles laid
@@ -67,10 +67,11 @@ struct Args {
   sap_step_args a;
   double *Tpart;   // [grid][r*m]
   double *t;       // [r*m]
+  unsigned *done;  // [1] CTAs of stage 2 finished (zeroed; reset by the last one)
   int parts;      // partials T_k (stage 0's grid)
   int rows_per;    // block rows per CTA
   int do_grad, do_apply, has_next;
-  int stage;       // 0: A+B, 1: C, 2: D, 3: E (one launch each, stream-ordered)
+  int stage;       // 0: A+B, 2: D (+E); C is phase4_reduce_kernel
   int dbg;         // profiling: 5 skips B's product, 6 D's product, 7 the update
 };
 
@@ -188,7 +189,6 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
 
   if (A.stage == 0) {
     // ---------------- A + B: gradient rows, partial U^T g ----------------
-    if (A.has_next && blockIdx.x == 0 && tid == 0) a.zflag[a.flag_idx ^ 1] = 0;
     double *Tk = A.Tpart + int64_t(blockIdx.x) * rm;
     if (woodbury && i1 <= i0)
       for (int o = tid; o < rm; o += kThreads) Tk[o] = 0.0;
@@ -234,44 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
     return;
   }
 
-  if (A.stage == 1) {
-    // ---------------- C: t = sum_k T_k (fixed order) ----------------
-    // sixteen lanes per output, each summing every sixteenth partial (loads
-    // issued ten at a time), combined in a fixed shuffle tree
-    constexpr int kL = 16, kU = 10;
-    const int64_t x = int64_t(blockIdx.x) * kThreads + tid;
-    const int64_t o = x / kL;
-    const int q = int(x % kL);
-    const int parts = A.parts;
-    double s = 0.0;
-    if (o < rm)
-      for (int k0 = q; k0 < parts; k0 += kL * kU) {
-        double v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int k = k0 + kL * u;
-          v[u] = k < parts ? __ldcg(A.Tpart + int64_t(k) * rm + o) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) s += v[u];
-      }
-#pragma unroll
-    for (int w = 1; w < kL; w <<= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
-    if (q == 0 && o < rm) A.t[o] = s;
-    return;
-  }
-
-  if (A.stage == 3) {
-    // ---------------- E: rebuild the next operand if its scale was left ----------------
-    if (*reinterpret_cast<volatile int *>(a.zflag + a.flag_idx) == 0) return;
-    zop::Next zn{a.Pw, a.Qw, a.ldp, a.n_local, m, float(a.zp1), float(a.zq1), a.Pb, a.Qb,
-                 static_cast<__half *>(a.Zhi_next), static_cast<__half *>(a.Zlo_next), a.ldz,
-                 a.zscale_next};
-    zop::next_pass(zn, blockIdx.x, gridDim.x, tid, kThreads);
-    return;
-  }
-
   // ---------------- D: D = g - UMc t, block update ----------------
+  if (A.has_next && blockIdx.x == 0 && tid == 0) a.zflag[a.flag_idx ^ 1] = 0;
   const double eta = (a.Pw && a.eta_dev) ? a.eta_dev[0] : 0.0;
   const double dsc = a.dscale_dev ? 1.0 / a.dscale_dev[0] : 1.0;
   for (int c = tid; c < 2 * m; c += kThreads) sbound[c] = 0.0f;
@@ -392,7 +356,57 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
     if (a.Qb && a.Qw && sbound[m + c] > 0.0f)
       atomicMax(reinterpret_cast<int *>(a.Qb + c), __float_as_int(sbound[m + c]));
   }
-  if (A.has_next && __syncthreads_or(over) && tid == 0) atomicOr(a.zflag + a.flag_idx, 1);
+  if (!A.has_next) return;
+  if (__syncthreads_or(over) && tid == 0) atomicOr(a.zflag + a.flag_idx, 1);
+  // ---------------- E: rebuild the next operand if its scale was left ----------------
+  // The last CTA to finish reads the flag (threadfence reduction pattern). The
+  // scale leaves 64x headroom (zop::scale), so this is a rare slow path: one
+  // CTA streams the whole operand.
+  __shared__ int last;
+  if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(A.done, 1u) == gridDim.x - 1;
+    if (last) {
+      atomicExch(A.done, 0u);
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (!last || *reinterpret_cast<volatile int *>(a.zflag + a.flag_idx) == 0) return;
+  zop::Next zn{a.Pw, a.Qw, a.ldp, a.n_local, m, zp1, zq1, a.Pb, a.Qb,
+               static_cast<__half *>(a.Zhi_next), static_cast<__half *>(a.Zlo_next), a.ldz,
+               a.zscale_next};
+  zop::next_pass(zn, 0, 1, tid, kThreads);
+}
+
+// ---------------- C: t = sum_k T_k (fixed order) ----------------
+// sixteen lanes per output, each summing every sixteenth partial (loads issued
+// ten at a time), combined in a fixed shuffle tree; a light kernel (few
+// registers) so its CTAs are resident and waiting while stage 0 finishes
+__global__ void __launch_bounds__(kThreads, 2) phase4_reduce_kernel(const Args A) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int kL = 16, kU = 10;
+  const int rm = A.a.r * A.a.m;
+  const int64_t x = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t o = x / kL;
+  const int q = int(x % kL);
+  const int parts = A.parts;
+  double s = 0.0;
+  if (o < rm)
+    for (int k0 = q; k0 < parts; k0 += kL * kU) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int k = k0 + kL * u;
+        v[u] = k < parts ? __ldcg(A.Tpart + int64_t(k) * rm + o) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) s += v[u];
+    }
+#pragma unroll
+  for (int w = 1; w < kL; w <<= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
+  if (q == 0 && o < rm) A.t[o] = s;
 }
 
 }  // namespace p4
@@ -478,6 +492,7 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
   // stages, each one launch in stream order; programmatic dependent launch
   // lets the next stage's grid be scheduled while the previous one runs (it
   // waits in griddepcontrol.wait), so the launch gaps between them shrink
+  A.done = static_cast<unsigned *>(ws);
   auto launch = [&](int stage, int grid, size_t sm) -> int {
     A.stage = stage;
     cudaLaunchConfig_t cfg{};
@@ -490,7 +505,8 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = getenv("SAP_P4_NO_PDL") ? 0 : 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, p4::phase4_kernel, A);
+    const cudaError_t e = stage == 1 ? cudaLaunchKernelEx(&cfg, p4::phase4_reduce_kernel, A)
+                                     : cudaLaunchKernelEx(&cfg, p4::phase4_kernel, A);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(SAP_ERR_DEVICE, "block_step: stage %d launch failed: %s", stage,
@@ -504,7 +520,6 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
   if (woodbury && (rc = launch(1, int((rm * 16 + p4::kThreads - 1) / p4::kThreads), 0)) != SAP_OK)
     return rc;
   if ((rc = launch(2, G, smem)) != SAP_OK) return rc;
-  if (has_next && (rc = launch(3, 2 * G, 0)) != SAP_OK) return rc;
   return SAP_OK;
 }
 

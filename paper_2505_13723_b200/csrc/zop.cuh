@@ -13,14 +13,18 @@
 namespace sap {
 namespace zop {
 
-// scale_c = 2^floor(log2(16384 / bound_c)) from per-column magnitude bounds:
-// the column's largest value maps into [8192, 16384], 4x below fp16's maximum.
+// scale_c = 2^floor(log2(1024 / bound_c)) from per-column magnitude bounds:
+// the column's largest value maps into [512, 1024], 64x below fp16's maximum,
+// so an operand whose scale was fixed before an update stays finite unless a
+// column grows 64x in one iteration. The headroom costs no precision that
+// matters: hi/lo keep 22 significant bits down to lo's subnormal floor of
+// 2^-24, i.e. 2^-34 of the column's largest value.
 // Rows c >= m (MMA padding) are not touched: the caller zeroes them once.
 __device__ __forceinline__ float scale(float zp, float zq, const float *Pb, const float *Qb,
                                        bool hasq, int c) {
   const float bound = fabsf(zp) * Pb[c] + (hasq ? fabsf(zq) * Qb[c] : 0.0f);
   float sc = 1.0f;
-  if (bound > 0.0f && isfinite(bound)) sc = exp2f(floorf(log2f(16384.0f / bound)));
+  if (bound > 0.0f && isfinite(bound)) sc = exp2f(floorf(log2f(1024.0f / bound)));
   return fminf(fmaxf(sc, 0x1p-100f), 0x1p100f);
 }
 
