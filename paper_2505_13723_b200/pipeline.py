@@ -125,10 +125,11 @@ class _Batch:
 
 
 class Lookahead:
-    """Produces IterPlan(t) for t = 0..total-1 in batches of ``L``."""
+    """Produces IterPlan(t) for t = start..total-1 (total None: unbounded) in
+    batches of up to ``L``."""
 
     def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
-                 tcp=None):
+                 tcp=None, start=0):
         self.o, self.shard, self.seed = oracle, shard, int(seed)
         if not 0 <= self.seed < 2**64:
             raise ContractError("seed must be a non-negative integer below 2**64")
@@ -147,7 +148,9 @@ class Lookahead:
         # batch before last, not the last one
         self.nslots = self.depth + 1 + max(0, int(os.environ.get("SAP_SPARE_SLOTS", "1")))
         cap = max(1, int(4e9 // (self.nslots * 4 * b * b)))
-        self.total, self.L = total, max(1, min(L, total, cap))
+        # total None: unbounded (the per-step API); batches are defined lazily
+        self.total = total
+        self.L = max(1, min(L, cap) if total is None else min(L, total, cap))
         self.iters = power_iters
         dev = oracle.device
         self.dev = dev
@@ -199,12 +202,10 @@ class Lookahead:
                 _l, _ = torch.linalg.cholesky_ex(_a)
                 torch.cholesky_inverse(_l)
                 torch.linalg.solve_triangular(_l, _a, upper=False)
-        # batch k covers iterations [bounds[k], bounds[k+1])
-        self.bounds = [0]
-        c = 1
-        while self.bounds[-1] < total:
-            self.bounds.append(min(total, self.bounds[-1] + c))
-            c = min(2 * c, self.L)
+        # batch k covers iterations [bounds[k], bounds[k+1]); sizes ramp 1, 2,
+        # 4, ... up to L, extended on demand (_has_batch)
+        self.bounds = [int(start)]
+        self._c = 1
         # depth producers: a batch's production (host RNG -> sketch on the GPU ->
         # host factorisation -> power iteration) takes longer than consuming
         # one, so depth batches are produced concurrently (slots k mod depth+1)
@@ -237,8 +238,17 @@ class Lookahead:
         self.cur = None
         self.k = -1  # batch currently consumed
         self.futs = {}
-        for k in range(min(self.depth, len(self.bounds) - 1)):
-            self._submit(k)
+        for k in range(self.depth):
+            if self._has_batch(k):
+                self._submit(k)
+
+    def _has_batch(self, k):
+        """Define batches up to k (lazily); False past the iteration budget."""
+        while len(self.bounds) <= k + 1 and (self.total is None or self.bounds[-1] < self.total):
+            nxt = self.bounds[-1] + self._c
+            self.bounds.append(nxt if self.total is None else min(self.total, nxt))
+            self._c = min(2 * self._c, self.L)
+        return len(self.bounds) > k + 1
 
     def _submit(self, k):
         t0, t1 = self.bounds[k], self.bounds[k + 1]
@@ -263,13 +273,16 @@ class Lookahead:
                 ev = torch.cuda.Event()
                 ev.record(main)
                 cur.slot.free = ev  # batch k+2 refills this slot after it
+            if not self._has_batch(self.k + 1):
+                raise ContractError(f"iteration {t} is past the solver's iteration budget "
+                                    f"({self.total})")
             self.k += 1
             cur = self.futs.pop(self.k).result()
             main.wait_event(cur.ready)
             if self.shard.world > 1:
                 self._share(cur)
             self.cur = cur
-            if self.k + self.depth < len(self.bounds) - 1:
+            if self._has_batch(self.k + self.depth):
                 self._submit(self.k + self.depth)
         i = t - cur.t0
         s = cur.slot

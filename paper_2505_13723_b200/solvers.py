@@ -255,29 +255,98 @@ def _basis(beta, alpha):
 
 
 class SolverState:
-    """Iterate state of ADASAP. ``W``, ``V`` and ``Z`` materialise on demand
-    (numpy, float64) from the device-resident lazy form."""
+    """Iterate triple of ADASAP (solvers.py:189-202): ``W``, ``V``, ``Z`` (n x m)
+    and ``iteration``; V and Z alias W when acceleration is off (``zeros``).
 
-    def __init__(self, engine):
-        self._e = engine
+    Drop-in semantics: a state made by ``SolverState.zeros`` (or from any
+    arrays) is stepped by ``adasap_step`` like the reference's. The first step
+    binds a device engine to the state (the lazy two-array form of DESIGN.md
+    §4, resumed from the state's arrays at ``iteration``); later steps reuse
+    it while the oracle, Y, config, accel and identity_precond are the same.
+    ``W``/``V``/``Z`` are written back lazily: reading one materialises the
+    current iterate as a fresh float64 host array (the reference rebinds them
+    to new arrays each step too, solvers.py:399-401). Assigning one, or
+    ``iteration``, detaches the engine; the next step resumes from the
+    assigned values."""
+
+    def __init__(self, W=None, V=None, Z=None, iteration=0):
+        if isinstance(W, AdasapEngine):  # bound to an engine (make_state)
+            self._e, self._W, self._V, self._Z, self._it = W, None, None, None, W.t
+            return
+        self._e = None
+        self._W, self._V, self._Z, self._it = W, V, Z, int(iteration)
+
+    @classmethod
+    def zeros(cls, n, m, accelerated=False):
+        W = np.zeros((n, m))
+        if accelerated:
+            return cls(W, W.copy(), W.copy())
+        return cls(W, W, W)
+
+    # -- engine binding ---------------------------------------------------------
+    def _sync(self):
+        """Host arrays <- the bound engine's current iterate."""
+        e = self._e
+        if e is not None and self._W is None:
+            vec = e.vector
+            self._W = _to_host64(e.gather_full(e.materialize("W")))
+            self._V = _to_host64(e.gather_full(e.materialize("V")))
+            self._Z = _to_host64(e.gather_full(e.materialize("Z")))
+            if vec:
+                self._W, self._V, self._Z = self._W[:, 0], self._V[:, 0], self._Z[:, 0]
+
+    def _detach(self):
+        self._sync()
+        if self._e is not None:
+            self._it = self._e.t
+            self._e.close()
+            self._e = None
 
     @property
     def iteration(self):
-        return self._e.t
+        return self._e.t if self._e is not None else self._it
 
-    # widened to float64 and made row-major on the device, so the host gets one
-    # contiguous copy (no host-side conversion of an n x m array)
+    @iteration.setter
+    def iteration(self, t):
+        self._detach()
+        self._it = int(t)
+
     @property
     def W(self):
-        return _to_host64(self._e.materialize("W"))
+        self._sync()
+        return self._W
+
+    @W.setter
+    def W(self, v):
+        self._detach()
+        self._W = v
 
     @property
     def V(self):
-        return _to_host64(self._e.materialize("V"))
+        self._sync()
+        return self._V
+
+    @V.setter
+    def V(self, v):
+        self._detach()
+        self._V = v
 
     @property
     def Z(self):
-        return _to_host64(self._e.materialize("Z"))
+        self._sync()
+        return self._Z
+
+    @Z.setter
+    def Z(self, v):
+        self._detach()
+        self._Z = v
+
+
+def _as2d(A):
+    if torch.is_tensor(A):
+        return A if A.ndim == 2 else A[:, None]
+    A = np.asarray(A, dtype=np.float64)
+    return A if A.ndim == 2 else A[:, None]
 
 
 def _to_host64(t):
@@ -299,7 +368,12 @@ def _to_host64(t):
 class AdasapEngine:
     """Device-resident ADASAP iteration (solvers.py:361-456)."""
 
-    def __init__(self, oracle, Y, config, accel, identity_precond=False, total=None, shard=None):
+    def __init__(self, oracle, Y, config, accel, identity_precond=False, total=None, shard=None,
+                 start=0, unbounded=False, state=None):
+        """``total``: iteration budget (default from the config); ``unbounded``
+        for the per-step API (adasap_step), which has no budget; ``start`` and
+        ``state`` = (W, V, Z) (n x m, host or device) resume from an iterate
+        triple at iteration ``start`` instead of zeros."""
         if not isinstance(oracle, KernelOracle):
             raise ContractError("the B200 solver needs a device KernelOracle")
         self.o = oracle
@@ -319,7 +393,11 @@ class AdasapEngine:
         self.b = resolve_blocksize(config, n)
         self.r = 0 if identity_precond else resolve_rank(config, self.b)
         self.lam = oracle.lam
-        self.total = total if total is not None else budget_iterations(config, self.b / n)
+        self.start = int(start)
+        self.total = None if unbounded else (total if total is not None else
+                                             budget_iterations(config, self.b / n))
+        self.accel_key = (accel.beta, accel.gamma, accel.alpha)
+        self.identity_precond = identity_precond
         beta, gamma, alpha = accel.beta, accel.gamma, accel.alpha
         self.beta, self.gamma, self.alpha = beta, gamma, alpha
         self.u1, self.u2, self.lam2, self.dense = _basis(beta, alpha)
@@ -338,7 +416,7 @@ class AdasapEngine:
         self.g = torch.empty((b, m), dtype=torch.float64, device=self.dev)
         self.WB = torch.zeros((b, m), dtype=f32, device=self.dev)
         self.last_loc = None
-        self.etas = torch.zeros(max(self.total, 1), dtype=torch.float64, device=self.dev)
+        self.etas = torch.zeros(max(self.total or 64, 1), dtype=torch.float64, device=self.dev)
         self.use_tc = oracle.use_tc(m) and b >= 16 and nl > 0 and not self.dense
         if self.use_tc:
             self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi)
@@ -368,10 +446,34 @@ class AdasapEngine:
             if free > 2 * self.zop.hi.numel() * 2 + (4 << 30):
                 self.zop_next = ZOperand(m, nl, self.dev)
         self.z_stale = True  # zop does not hold Z_t yet (filled by the first step)
-        self.t = 0
+        self.t = self.start
+        self.W0 = None  # W at `start` when resuming from a nonzero state (until the first step)
+        if state is not None:
+            self._load_state(*state)
         self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
-                            config.lookahead, identity_precond, tcp=self.tcp)
+                            config.lookahead, identity_precond, tcp=self.tcp, start=self.start)
         self.crcs = []
+
+    def _load_state(self, W, V, Z):
+        """[V; Z] = M [P; Q] row-wise from a given iterate triple."""
+        sh, nl = self.shard, self.shard.size
+        if nl == 0:
+            return
+        cm = lambda A: to_colmajor(A[sh.lo:sh.hi] if A.ndim == 2 else A[sh.lo:sh.hi, None], nl,
+                                   self.dev, self.ld)
+        Vd, Zd = cm(_as2d(V)), cm(_as2d(Z))
+        (a, b), (c, d) = self.M
+        det = a * d - b * c
+        # [P; Q] = M^-1 [V; Z], fp32 on the device
+        self.P.copy_(Vd * (d / det) - Zd * (b / det))
+        self.Q.copy_(Zd * (a / det) - Vd * (c / det))
+        self.W0 = cm(_as2d(W))[:, :nl].T.contiguous()
+        if self.Pb is not None:
+            for A, bnd in ((self.P, self.Pb), (self.Q, self.Qb)):
+                nat.call("sap_colabsmax", nat.ptr(A), A.stride(0), nl, self.m, nat.ptr(bnd),
+                         nat.stream_handle())
+        if self.dense:
+            self.Wdense = self.W0.clone()
 
     def close(self):
         self.la.close()
@@ -418,7 +520,7 @@ class AdasapEngine:
             D = self.g
         self._update(plan, D)
         if self.t == plan.batch_t0:  # the batch's stepsizes into the trace, once per batch
-            self.etas[self.t:self.t + plan.batch_eta.numel()].copy_(plan.batch_eta)
+            self._record_etas(plan)
         self.last_loc = plan.loc_dev
         self.crcs.append(plan.crc)
         self.t += 1
@@ -485,11 +587,30 @@ class AdasapEngine:
             self.z_stale = True
         self._advance(s_next)
         if self.t == plan.batch_t0:  # the batch's stepsizes into the trace, once per batch
-            self.etas[self.t:self.t + plan.batch_eta.numel()].copy_(plan.batch_eta)
+            self._record_etas(plan)
         self.last_loc = plan.loc_dev
         self.crcs.append(plan.crc)
         self.t += 1
         return plan
+
+    def eval_point(self, config):
+        """The block-row product's point (solvers.py:376): None for Z (the
+        engine's own operand), else W as a column-major (m x ld) array."""
+        if config.grad_eval_point != "w" or (self.t == self.start and self.W0 is None):
+            return None  # W = Z = 0 before the first step of a fresh solve
+        W = self.materialize("W").T
+        pt = torch.zeros((self.m, self.ld), dtype=torch.float32, device=self.dev)
+        pt[:, :W.shape[1]] = W
+        return pt
+
+    def _record_etas(self, plan):
+        k0, k1 = self.t - self.start, self.t - self.start + plan.batch_eta.numel()
+        if k1 > self.etas.numel():
+            grown = torch.zeros(max(k1, 2 * self.etas.numel()), dtype=torch.float64,
+                                device=self.dev)
+            grown[:self.etas.numel()].copy_(self.etas)
+            self.etas = grown
+        self.etas[k0:k1].copy_(plan.batch_eta)
 
     def _coeffs(self):
         """(e0, e1, s_next): the block rows' update of [P; Q] in the next basis,
@@ -548,7 +669,9 @@ class AdasapEngine:
         nl = self.shard.size
         out = torch.empty((self.m, self.ld), dtype=torch.float32, device=self.dev)
         if which == "W":
-            if self.t == 0:
+            if self.t == self.start:
+                if self.W0 is not None:
+                    return self.W0.clone()
                 return torch.zeros((nl, self.m), dtype=torch.float32, device=self.dev)
             a, c = self.M_prev[1, 0], self.M_prev[1, 1]
         elif which == "Z":
@@ -598,26 +721,60 @@ def _y_norm(Y):
     return max(nrm, np.finfo(np.float64).tiny)
 
 
-def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=False):
-    """One iteration on an engine-backed state (solvers.py:361-403).
+def _config_key(config):
+    return (config.seed, config.blocksize, config.nystrom_rank, config.grad_eval_point,
+            config.lookahead, config.lam)
 
-    ``state`` is a SolverState returned by ``make_state``; returns
-    (state, eta, block) like the reference (eta read back from the device)."""
-    eng = state._e
-    plan = eng.step()
-    # eta_t is produced ahead by the lookahead; reading it back does not wait
-    # for this step's block product (call torch.cuda.synchronize() or read W
-    # to wait for the iterate itself)
+
+def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=False):
+    """One iteration t = state.iteration (solvers.py:361-403); returns
+    (state, eta, block) like the reference.
+
+    ``state`` is a ``SolverState`` (e.g. ``SolverState.zeros(n, m, True)``).
+    Y, config, accel and identity_precond are read on every call: the device
+    engine bound to the state is reused only while they are the same (Y the
+    same array object); otherwise the state is written back and a new engine
+    resumes from it. ``pool`` is accepted for API compatibility (the device
+    runs all tiles in one launch). eta is read back from the device (its
+    lookahead batch is produced ahead, so this does not wait for the step's
+    block product; read ``state.W`` or synchronise to wait for the iterate)."""
+    if not isinstance(state, SolverState):
+        raise ContractError("adasap_step needs a SolverState")
+    e = state._e
+    key = (id(oracle), id(Y), _config_key(config), (accel.beta, accel.gamma, accel.alpha),
+           bool(identity_precond))
+    if e is None or getattr(e, "bind_key", None) != key:
+        state._detach()
+        n = oracle.n
+        if state._W is None:
+            raise ContractError("state has no iterate arrays")
+        for A in (state._W, state._V, state._Z):
+            if _as2d(A).shape[0] != n:
+                raise ContractError("state arrays must have n rows")
+        zero = all(not np.any(np.asarray(A)) if not torch.is_tensor(A) else not bool(A.any())
+                   for A in (state._W, state._V, state._Z))
+        e = AdasapEngine(oracle, Y, config, accel, identity_precond, unbounded=True,
+                         start=state._it,
+                         state=None if zero else (state._W, state._V, state._Z))
+        e.bind_key = key
+        e.Y_src = Y  # keeps id(Y) valid while bound
+        state._e = e
+    plan = e.step(e.eval_point(config))
+    state._W = state._V = state._Z = None  # written back lazily
     return state, plan.eta_host(), plan.block
 
 
 def make_state(oracle, Y, config, accel=None, identity_precond=False, total=None):
-    """Fresh zero state (solvers.py:197-202) bound to a device engine."""
+    """Fresh zero state (solvers.py:197-202) bound to a device engine with an
+    iteration budget (``total``, default from the config)."""
     n = oracle.n
     b = resolve_blocksize(config, n)
     if accel is None:
         accel = resolve_accel(config, n, b)
     eng = AdasapEngine(oracle, Y, config, accel, identity_precond, total)
+    eng.bind_key = (id(oracle), id(Y), _config_key(config), (accel.beta, accel.gamma, accel.alpha),
+                    bool(identity_precond))
+    eng.Y_src = Y
     return SolverState(eng)
 
 
@@ -639,13 +796,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
         done = 0
         pending = []  # (iteration, passes, relres, crc) -- stepsizes filled at the end
         for t in range(total):
-            point = eng.materialize("W").T.contiguous() if config.grad_eval_point == "w" and \
-                eng.t > 0 else None
-            if point is not None:
-                pt = torch.zeros((eng.m, eng.ld), dtype=torch.float32, device=eng.dev)
-                pt[:, :point.shape[1]] = point
-                point = pt
-            plan = eng.step(point)
+            plan = eng.step(eng.eval_point(config))
             done = t + 1
             W_loc = None
             if averager is not None or on_iterate is not None:

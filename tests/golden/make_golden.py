@@ -18,6 +18,12 @@ Fixtures (all float64, reference arithmetic):
                      inputs are regenerated from seeds by the tests
   randnla.npz        Nystrom factor, Woodbury applies, power stepsize
   rng.npz            block crc32s / first draws for several (seed, t, n, b)
+  config3.npz        config 3 (n=1e6, d=9, b=2000, m=65): one block product per
+                     family (Matern-3/2, RBF) and a 5-iteration Matern-3/2
+                     trajectory (block crc32s, stepsizes, sampled rows of W)
+  config2_traj.npz   config 2 (n=1e5, d=11 RBF, b=1000, m=65, pathwise RHS) for
+                     one pass (100 iterations): crc32s, stepsizes, sampled rows
+                     of W, posterior mean and test RMSE
   baselines.npz      the exact-SAP, SDD and Nystrom-PCG solvers (solvers.py:269-584) on
                      the config 1 problem: final estimates, residual traces,
                      block crc32s
@@ -186,13 +192,84 @@ def rng_fixture():
                         omega=om, power=pw)
 
 
+# rows of W kept in the trajectory fixtures (a deterministic sample: the full
+# n x m iterate does not fit a fixture)
+def sample_rows(n, k=4096):
+    return np.sort(substream(0, "golden_rows", n).choice(n, min(k, n), replace=False))
+
+
+def config3():
+    """Config 3 (the headline shape: n=1e6, d=9, b=2000, m=65) from the live
+    reference: one block product per family (Matern-3/2 and RBF) and a
+    5-iteration ADASAP trajectory (Matern-3/2, r=100, noise right-hand sides
+    regenerated from a named substream)."""
+    out = {}
+    n, d, b, m, seed = 1_000_000, 9, 2000, 65, 0
+    X = synthetic.make_inputs(n, d, seed)
+    Z = substream(seed, "golden_z3").standard_normal((n, m))
+    pool = sapgp.WorkerPool(8)
+    for fam in ("matern32", "rbf"):
+        spec = sapgp.KernelSpec(fam, np.full(d, np.sqrt(d)), 1.0)
+        orc = sapgp.KernelOracle(spec, X, 1e-2)
+        B = rsol._uniform_block(seed, 0, n, b)
+        out[f"{fam}_B"] = B
+        out[f"{fam}_G"] = rdist.col_dist_matmul(orc, Z, B, pool)
+    del Z
+    # 5 iterations of the reference solver
+    spec = sapgp.KernelSpec("matern32", np.full(d, np.sqrt(d)), 1.0)
+    orc = sapgp.KernelOracle(spec, X, 1e-2)
+    Y = substream(seed, "golden_y3").standard_normal((n, m))
+    cfg = sapgp.RunConfig(lam=1e-2, blocksize=b, nystrom_rank=100, residual_every=0, seed=seed,
+                          max_iters=5)
+    res = rsol.adasap_solve(orc, Y, cfg, pool=pool)
+    rows = sample_rows(n)
+    out["traj_rows"] = rows
+    out["traj_W_rows"] = res.W[rows]
+    out["traj_W_colnorm"] = np.linalg.norm(res.W, axis=0)
+    out["traj_crc"] = np.array([rec.block_hash for rec in res.trace.records], dtype=np.int64)
+    out["traj_eta"] = np.array([rec.stepsize for rec in res.trace.records])
+    pool.close()
+    np.savez_compressed(os.path.join(HERE, "config3.npz"), **out)
+
+
+def config2_trajectory():
+    """Config 2 (houseelec-shaped: n=1e5, d=11, RBF, b=1000, m=65, pathwise
+    right-hand sides built on the host) for one pass (100 iterations) of the
+    live reference: block crc32s, stepsizes, sampled rows of W, the posterior
+    mean at the test points and its test RMSE."""
+    n, d, b, m, seed, lam = 100_000, 11, 1000, 65, 0, 1e-2
+    prob = synthetic.make_problem(n, d, "rbf", m, seed=seed, lam=lam)
+    spec = sapgp.KernelSpec("rbf", prob.lengthscales, prob.variance)
+    orc = sapgp.KernelOracle(spec, prob.X, lam)
+    cfg = sapgp.RunConfig(lam=lam, blocksize=b, nystrom_rank=100, residual_every=0, seed=seed,
+                          max_passes=1.0)
+    pool = sapgp.WorkerPool(8)
+    res = rsol.adasap_solve(orc, prob.Y, cfg, pool=pool)
+    pool.close()
+    rows = sample_rows(n)
+    pm = orc.cross_matmul(prob.Xtest, res.W)
+    out = dict(rows=rows, W_rows=res.W[rows], W_colnorm=np.linalg.norm(res.W, axis=0),
+               crc=np.array([rec.block_hash for rec in res.trace.records], dtype=np.int64),
+               eta=np.array([rec.stepsize for rec in res.trace.records]),
+               iters=np.array(res.iterations), test_mean=pm,
+               test_rmse=np.array(sapgp.rmse(pm[:, 0], prob.ytest)),
+               Y_colnorm=np.linalg.norm(prob.Y, axis=0))
+    np.savez_compressed(os.path.join(HERE, "config2_traj.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     kernels_small()
     config1()
     baselines()
     config2()
     randnla()
     rng_fixture()
+    config3()
+    config2_trajectory()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

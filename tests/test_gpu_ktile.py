@@ -1,7 +1,8 @@
 """The batched K_BB tile (sap_ktile_f32_batch, the lookahead's power-iteration
-input) against the per-block tile kernel (sap_ktile_f32, itself checked
-against the oracle's KernelOracle.block in test_gpu_parity.py): same values
-bit for bit, one launch per batch."""
+input) against the per-block tile kernel sap_ktile_f32: same values bit for
+bit, one launch per batch. Both are checked against the CPU oracle's
+block_block (KernelOracle.block, kernels.py:129-136) at the headline shape in
+tests/test_gpu_config3.py::test_hot_path_kbb_tile_matches_oracle."""
 import numpy as np
 import pytest
 
