@@ -24,6 +24,7 @@
  *   sap_pq_update       <- nesterov_update on the block rows    solvers.py:76-85, :397-401
  *   sap_woodbury_apply  <- apply_inv (Nystrom-Woodbury)         randnla.py:109-134
  *   sap_block_step      <- Phases I(tail)-IV of adasap_step     solvers.py:376-401
+ *   sap_sym_eig_batch   <- the SVD / eigh of rand_nystrom        randnla.py:52-94
  *   sap_combine         <- materialising W (or Z) from the lazy
  *                          two-array Nesterov state
  *   sap_sdd_update      <- sdd_solve's momentum/averaging step  solvers.py:487-493
@@ -384,6 +385,23 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
                       const float *Q, int64_t ldp, double zp, double zq, const float *Pb,
                       const float *Qb, void *Zhi_next, void *Zlo_next, float *zscale_next,
                       void *stream);
+
+/* ---- batched symmetric eigensolver (jacobi.cu) ------------------------- */
+
+/*
+ * Eigen-decomposition of `count` symmetric r x r fp64 matrices (A[q] at
+ * A + q*strideA, row stride lda; symmetrised, then destroyed) by cyclic
+ * two-sided Jacobi, one CTA per matrix: evals[q*r + k] descending and the
+ * matching eigenvectors as columns of V[q] (V + q*strideV, row stride ldv).
+ * sweeps[q] (nullable) = sweeps used, -1 if max_sweeps did not converge.
+ * Replaces np.linalg.eigh on the Nystrom Gram matrices (the Gram route of
+ * rand_nystrom, randnla.py:52-94). Workspace: sap_sym_eig_workspace (0 when
+ * the matrices fit shared memory, r <= 112).
+ */
+size_t sap_sym_eig_workspace(int r, int count);
+int sap_sym_eig_batch(double *A, int64_t strideA, int lda, int r, int count, double *evals,
+                      double *V, int64_t strideV, int ldv, int max_sweeps, int *sweeps,
+                      void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

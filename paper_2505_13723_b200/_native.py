@@ -74,6 +74,8 @@ SIGNATURES = {
     "sap_block_step_workspace": (_SZ, [_I64, _I, _I]),
     "sap_block_step": (_I, [_P, _I, _P, _SZ, _P]),
     "sap_woodbury_apply": (_I, [_P, _P, _I64, _I64, _I, _P, _I64, _I, _P, _P, _I64, _P, _SZ, _P]),
+    "sap_sym_eig_workspace": (_SZ, [_I, _I]),
+    "sap_sym_eig_batch": (_I, [_P, _I64, _I, _I, _I, _P, _P, _I64, _I, _I, _P, _P, _SZ, _P]),
 }
 
 

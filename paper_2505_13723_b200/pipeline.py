@@ -16,12 +16,13 @@ threads, up to ``depth`` batches ahead of the block-row products that
 consume them; their GPU work is enqueued in order on the solver's stream
 (see Lookahead.__init__). Batch sizes ramp 1, 2, 4, ... up to
 ``L = config.lookahead`` so the first iteration waits for one plan only, not
-for a full batch. Per batch there is one device->host round trip: the r x r
-matrices whose symmetric eigensolves run on the host workers (LAPACK beats the
-GPU's batched eigensolver at r = 100); the rest of the factorisation (the
-shift ladder's Cholesky factors, the Woodbury core, rho) and everything
-dimension-b runs on the GPU (``randnla.factor_gram_batch``; Omega, the
-sketch, U = Y W, K[B,B], the batched power iteration). Buffers
+for a full batch. The host draws the blocks (numpy-exact, csrc/host_rng.cu)
+and enqueues; everything else runs on the GPU with no device->host round
+trip: Omega, the sketch, the Gram matrices, the whole r x r factorisation
+(shift ladder, Jacobi eigensolves, Woodbury core, rho;
+``randnla.factor_gram_batch``), U = Y W, K[B,B] and the batched power
+iteration. Failures the reference raises at the failing step are flagged on
+the device and raised by ``check_flags``. Buffers
 live in depth + 1 preallocated slots reused under CUDA events, so nothing is
 allocated in steady state.
 """
@@ -41,7 +42,8 @@ import torch
 from . import kernels as K
 from .errors import NumericalError
 from .errors import ContractError
-from .randnla import FactorFailure, factor_gram_batch
+from .randnla import (FLAG_CHOLESKY, FLAG_EIGH, FLAG_EXTRA_SHIFT, FLAG_NEG_TRACE, FLAG_PLAIN,
+                      FLAG_POWER, factor_gram_batch)
 from .rng import DeviceNormals
 
 
@@ -210,31 +212,21 @@ class Lookahead:
         # host factorisation -> power iteration) takes longer than consuming
         # one, so depth batches are produced concurrently (slots k mod depth+1)
         self.pool = ThreadPoolExecutor(max_workers=self.depth, thread_name_prefix="sap-lookahead")
-        # host workers for the per-iteration numpy RNG and r x r LAPACK work (both
-        # release the GIL in their kernels); sized to leave cores for the main thread
+        # host threads of the native block draws (sap_host_draws, GIL released);
+        # sized to leave cores for the main thread
         try:
             cores = len(os.sched_getaffinity(0))
         except AttributeError:  # pragma: no cover
             cores = os.cpu_count() or 1
         self.host_threads = max(1, min(self.L, cores - 2, 8))
-        self.hostpool = ThreadPoolExecutor(max_workers=self.host_threads,
-                                           thread_name_prefix="sap-host")
         self.timings = [] if os.environ.get("SAP_PROFILE") else None
-        # The solver thread enqueues ~20 launches per iteration and must keep
-        # ahead of the device while the producer and host workers run Python
-        # between their numpy/LAPACK calls: with CPython's default 5 ms GIL
+        # The solver thread enqueues its launches and must keep ahead of the
+        # device while the producer threads run Python: with CPython's default 5 ms GIL
         # switch interval it can wait a whole interval for the GIL, longer than
         # an iteration's device time. 0.2 ms bounds that wait.
         swi = float(os.environ.get("SAP_SWITCH_INTERVAL", "2e-4"))
         if sys.getswitchinterval() > swi:
             sys.setswitchinterval(swi)
-        # r x r LAPACK calls from several host workers: one BLAS thread each (the
-        # reference pins BLAS to one thread for the same reason, __init__.py:16-22)
-        try:
-            from threadpoolctl import threadpool_limits
-            self._blas_limit = threadpool_limits(limits=1, user_api="blas")
-        except Exception:  # pragma: no cover - threadpoolctl is optional
-            self._blas_limit = None
         self.cur = None
         self.k = -1  # batch currently consumed
         self.futs = {}
@@ -259,10 +251,6 @@ class Lookahead:
 
     def close(self):
         self.pool.shutdown(wait=True)
-        self.hostpool.shutdown(wait=True)
-        if self._blas_limit is not None:
-            self._blas_limit.restore_original_limits()
-            self._blas_limit = None
 
     # -- consumer side (main thread) ------------------------------------------
     def get(self, t):
@@ -340,14 +328,29 @@ class Lookahead:
             cur.eta_ready = ev
 
     def check_flags(self):
-        """Raise if any power iteration or device normal draw failed (checked once,
-        at the end)."""
+        """Raise the failures the reference raises at the failing step (device
+        RNG, factorisation, power iteration), and warn for the fallbacks;
+        checked once, at the end (flags are sticky per slot)."""
+        bits = 0
         for s in self.slots:
             if s.normals is not None and int(s.normals.status()) != 0:
                 raise NumericalError("device normal draw ran out of raw stream words")
-            if int(s.bad.max()) != 0:
-                raise NumericalError("power iteration failed (collapsed or nonpositive Rayleigh "
-                                     "estimate; H is not PSD)")
+            bits |= int(np.bitwise_or.reduce(s.bad.cpu().numpy()))
+        if bits & FLAG_NEG_TRACE:
+            raise NumericalError("sketch Gram has negative trace; M is not PSD")
+        if bits & FLAG_CHOLESKY:
+            raise NumericalError("Cholesky of the shifted Gram failed; retry with a larger shift")
+        if bits & FLAG_EIGH:
+            raise NumericalError("Jacobi eigensolver of the Nystrom Gram did not converge")
+        if bits & FLAG_POWER:
+            raise NumericalError("power iteration failed (collapsed or nonpositive Rayleigh "
+                                 "estimate; H is not PSD)")
+        if bits & FLAG_PLAIN:
+            warnings.warn("stabilized Woodbury Cholesky failed; falling back to the plain "
+                          "identity", RuntimeWarning)
+        if bits & FLAG_EXTRA_SHIFT:
+            warnings.warn("Nystrom Gram needed a shift beyond the reference ladder "
+                          "(SAP_EXTRA_SHIFTS=1)", RuntimeWarning)
 
     # -- producer side (worker thread) ------------------------------------------
     def _host_draws(self, slot, t0, count, omega, v0):
@@ -427,30 +430,19 @@ class Lookahead:
         tm2 = time.perf_counter()
         Ss = [None] * count
         if r:
-            # the r x r factorisations, batched on the device (fast stream); only
-            # the symmetric eigensolves go to the host workers (one sync)
+            # the r x r factorisations, batched on the device (fast stream), the
+            # eigensolves included (sap_sym_eig_batch): no host round trip;
+            # failures and warnings ride on the plan flags (check_flags)
             with torch.cuda.device(self.dev), torch.cuda.stream(fs):
-                def eigh_host(H):
-                    res = list(self.hostpool.map(np.linalg.eigh, H))
-                    return np.stack([x[0] for x in res]), np.stack([x[1] for x in res])
-                try:
-                    W, S, rho_d, Mc, E, plain = factor_gram_batch(
-                        G[:, :r, :r], G[:, r:, :r], G[:, r:, r:], r, self.lam, eigh_host)
-                except FactorFailure as exc:
-                    i = int(exc.args[0][0])
-                    if np.linalg.matrix_rank(slot.omega[i].cpu().numpy()) < r:
-                        raise ContractError("test matrix omega is rank deficient") from exc
-                    raise NumericalError("Cholesky of the shifted Gram failed at every shift") \
-                        from exc
+                W, S, rho_d, Mc, E, flags = factor_gram_batch(
+                    G[:, :r, :r], G[:, r:, :r], G[:, r:, r:], r, self.lam)
                 tm2 = time.perf_counter()
                 torch.bmm(Y, W, out=slot.U[:count])
                 slot.Mc[:count].copy_(Mc)
                 torch.bmm(slot.U[:count], Mc, out=slot.UMc[:count])
                 slot.E[:count, :r].copy_(E)
                 slot.rho[:count].copy_(rho_d)
-                if bool(plain.any()):
-                    warnings.warn("stabilized Woodbury Cholesky failed; falling back to the plain "
-                                  "identity", RuntimeWarning)
+                slot.bad[:count] |= flags
                 ev = torch.cuda.Event()
                 ev.record(fs)
         else:

@@ -24,6 +24,9 @@ Fixtures (all float64, reference arithmetic):
   config2_traj.npz   config 2 (n=1e5, d=11 RBF, b=1000, m=65, pathwise RHS) for
                      one pass (100 iterations): crc32s, stepsizes, sampled rows
                      of W, posterior mean and test RMSE
+  nystrom_failures.npz  rand_nystrom_retry outcomes (S, or the NumericalError
+                     message) on sketches of PSD, negative, indefinite and
+                     low-rank matrices
   baselines.npz      the exact-SAP, SDD and Nystrom-PCG solvers (solvers.py:269-584) on
                      the config 1 problem: final estimates, residual traces,
                      block crc32s
@@ -257,6 +260,39 @@ def config2_trajectory():
     np.savez_compressed(os.path.join(HERE, "config2_traj.npz"), **out)
 
 
+def nystrom_failures():
+    """rand_nystrom_retry (randnla.py:97-106) on sketches of indefinite /
+    negative matrices: which raise NumericalError (and which message), which
+    succeed after escalating, and their S."""
+    rng = np.random.default_rng(17)
+    b, r = 120, 20
+    out = {}
+    cases = []
+    A = rng.standard_normal((b, b))
+    psd = A @ A.T / b
+    ev, Q = np.linalg.eigh(psd)
+    cases.append(("psd", psd))
+    cases.append(("negdef", -psd))                                   # negative trace
+    ind = Q @ np.diag(np.where(np.arange(b) % 3 == 0, -ev, ev)) @ Q.T  # indefinite, tr > 0
+    cases.append(("indefinite", ind))
+    low = Q[:, -10:] @ np.diag(ev[-10:]) @ Q[:, -10:].T                # rank 10 < r
+    cases.append(("lowrank", low))
+    names = []
+    for k, (name, M) in enumerate(cases):
+        om = rng.standard_normal((b, r))
+        sk = M @ om
+        out[f"{name}_sketch"], out[f"{name}_omega"] = sk, om
+        try:
+            fac = rrand.rand_nystrom_retry(sk, om, r)
+            out[f"{name}_S"] = fac.S
+            out[f"{name}_error"] = np.array("")
+        except sapgp.NumericalError as exc:
+            out[f"{name}_error"] = np.array(str(exc))
+        names.append(name)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "nystrom_failures.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate only the named fixtures
         for name in sys.argv[1:]:
@@ -270,6 +306,7 @@ if __name__ == "__main__":
     rng_fixture()
     config3()
     config2_trajectory()
+    nystrom_failures()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

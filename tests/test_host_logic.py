@@ -131,7 +131,8 @@ def test_no_cpu_fallback_without_device(monkeypatch):
 
 def test_batched_device_factor_matches_host_factor():
     """randnla.factor_gram_batch (the lookahead's batched factorisation; run here
-    on CPU tensors) equals the per-element host path factor_gram_retry +
+    on CPU tensors with torch's eigh standing in for the device Jacobi solver,
+    which tests/test_gpu_fused_step.py checks against numpy) equals the per-element host path factor_gram_retry +
     woodbury_core + rho + the P^{-1/2} coefficients, including an element that
     needs a shift escalation and one with pruned null modes."""
     import torch
@@ -150,10 +151,11 @@ def test_batched_device_factor_matches_host_factor():
         trip.append((Y.T @ Y, Om.T @ Y, Om.T @ Om))
     G = [torch.as_tensor(np.stack([t[k] for t in trip])) for k in range(3)]
 
-    def eigh_host(H):
-        return np.linalg.eigh(H)
+    def eig(H):  # the device Jacobi eigensolver's contract: descending, sweeps
+        ev, V = torch.linalg.eigh(H)
+        return ev.flip(-1), V.flip(-1), torch.zeros(H.shape[0], dtype=torch.int32)
 
-    W, S, rho, Mc, E, plain = factor_gram_batch(G[0], G[1], G[2], r, lam, eigh_host)
+    W, S, rho, Mc, E, flags = factor_gram_batch(G[0], G[1], G[2], r, lam, eig=eig)
     for i, (gyy, goy, goo) in enumerate(trip):
         Wh, Sh, UtU = factor_gram_retry(gyy, goy, goo, r)
         rho_h = float(Sh[-1]) + lam
@@ -175,4 +177,4 @@ def test_batched_device_factor_matches_host_factor():
                                    atol=1e-9 * np.abs(Wh @ Mch @ Wh.T).max())
         np.testing.assert_allclose(E[i].numpy(), 1.0 / np.sqrt(Sh + rho_h) - 1.0 / np.sqrt(rho_h),
                                    rtol=1e-8, atol=1e-12)
-    assert not plain.any()
+    assert not flags.any()
