@@ -14,8 +14,13 @@ iteration). The per-iteration working set (X 48 MB + lazy state P, Q
 520 MB) exceeds the 126 MB L2, so no explicit flush is needed between steps.
 
 ``roofline`` describes the dominant kernel (the fused block-row product
-K[B,:]Z, sap_krows_times): algorithmic flops per launch = b * n_local *
-2 (d + m), timed with CUDA events on its stream.
+K[B,:]Z on the tensor cores, sap_krows_tc): algorithmic flops per launch =
+b * n_local * 2 (d + m), timed with CUDA events on its
+stream, against the measured bf16 peak / 3 (three
+split-precision passes per algorithmic flop); ``traffic`` is the DRAM bytes of
+one launch from the committed ncu capture. ``e2e`` runs reference-style code
+(SolverState.zeros + adasap_step) from host arrays with setup and the final
+readback inside the timed region, bytes counted at each copy.
 ``cpu_baseline`` is the CPU oracle port (oracle/sapgp_oracle.py, a numpy
 restatement of the reference) timed on this host's cores for one iteration.
 ``--impl reference`` times that same CPU implementation as the reference arm.
@@ -38,12 +43,6 @@ sys.path.insert(0, ROOT)
 # the CPU oracle runs one BLAS thread per worker (reference conftest / __init__ policy)
 for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
     os.environ.setdefault(_v, "1")
-
-# dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at this
-# config, from the committed ncu capture (profiles/); re-capture when the kernel changes.
-# dram__bytes_read.sum + dram__bytes_write.sum of one sap_krows_tc launch at config 3
-# (profiles/r01e_krows_tc2_*_ncu_summary.txt, ncu --set full)
-TRAFFIC_PER_LAUNCH = {"matern32": 416_395_008 + 21_179_392, "rbf": 416_449_280 + 19_812_352}
 
 CONFIG = dict(n=1_000_000, d=9, family="matern32", b=2000, m=65, r=100, lam=1e-2, seed=0)
 METRIC = "ADASAP iters/s & kernel-entries/s at n=1M,1/2/4/8 B200; time-to-target RMSE"
@@ -181,6 +180,24 @@ def b_pad_rows(b):
     return (b + 255) // 256 * 256  # block rows the CTA-pair kernel computes
 
 
+# The lookahead produces plans in batches that ramp 1, 2, 4, ..., 32 over the
+# first 63 iterations (pipeline.Lookahead); those iterations are not steady
+# state, so they count as warm-up whatever --warmup asks for.
+RAMP_ITERS = 64
+
+
+def measured_traffic(family):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one block-row launch at
+    this config, from the committed ncu capture (profiles/r02_krows_traffic.json,
+    written by scripts/ncu_traffic.py from an `ncu --set full` report of this
+    bench); None if that capture is absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_krows_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    return d.get(family)
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -189,7 +206,7 @@ def run_b200(args):
     import paper_2505_13723_b200 as sap
     from paper_2505_13723_b200 import _native as nat
     from paper_2505_13723_b200 import synthetic
-    from paper_2505_13723_b200.parallel import current_shard, init_from_env
+    from paper_2505_13723_b200.parallel import init_from_env
     from paper_2505_13723_b200.solvers import AdasapEngine
 
     dist = init_from_env("nccl")
@@ -204,11 +221,13 @@ def run_b200(args):
                                   seed=CONFIG["seed"], lam=CONFIG["lam"], device=dev)
     spec = prob.spec()
     oracle = sap.KernelOracle(spec, prob.X, prob.lam, device=dev)
-    total = args.warmup + args.steps
+    warm = max(args.warmup, RAMP_ITERS)
     cfg = sap.RunConfig(lam=prob.lam, blocksize=CONFIG["b"], nystrom_rank=CONFIG["r"],
-                        residual_every=0, seed=CONFIG["seed"], max_iters=total)
+                        residual_every=0, seed=CONFIG["seed"])
     accel = sap.resolve_accel(cfg, args.n, CONFIG["b"])
-    eng = AdasapEngine(oracle, prob.Y, cfg, accel, total=total + 8)
+    # unbounded: the lookahead keeps producing at its steady rate through the
+    # timed window, as inside a long solve
+    eng = AdasapEngine(oracle, prob.Y, cfg, accel, unbounded=True)
     shard = eng.shard
     n_local = shard.size
     b, m, d = CONFIG["b"], CONFIG["m"], CONFIG["d"]
@@ -216,7 +235,7 @@ def run_b200(args):
     sampler = ClockSampler(local)
     if os.environ.get("SAP_BENCH_NO_CLOCKS") != "1":  # diagnosis only
         sampler.start()
-    for _ in range(args.warmup):
+    for _ in range(warm):
         eng.step()
     torch.cuda.synchronize()
 
@@ -268,33 +287,19 @@ def run_b200(args):
     entries = b * args.n
     flops_launch = b * n_local * 2 * (d + m)
     achieved = flops_launch / (kmean * 1e-3) / 1e12
-    kernel_name = ("sap_krows_tc (tcgen05 + TMEM + TMA, split-precision)" if eng.use_tc
+    kernel_name = ("sap_krows_tc (tcgen05 + TMEM + TMA, 3-pass split precision)" if eng.use_tc
                    else "sap_krows_times (FFMA path)")
-
-    # FP32 FFMA peak of this GPU (the FFMA path's denominator)
-    buf = torch.zeros(256, device=dev)
-    iters = 1 << 16
-    nat.call("sap_ffma_peak", nat.ptr(buf), iters, nat.stream_handle())
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    nat.call("sap_ffma_peak", nat.ptr(buf), iters, nat.stream_handle())
-    e1.record()
-    torch.cuda.synchronize()
-    ffma_peak = 148 * 4 * 256 * 8 * iters * 2 / (e0.elapsed_time(e1) * 1e-3) / 1e12
-    lib_launches_after = lib.sap_launch_count()
 
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
-
     bf16_peak = float(peaks.get("bf16_tflops", 1590.0))
-    # What the tensor pipe must execute per kernel entry in this formulation
-    # (DESIGN.md §5): GEMM1 kind::tf32 over the ka augmented features, GEMM2
-    # kind::f16 three split passes over nz padded right-hand sides. tf32 dense
-    # peak taken as half the measured bf16 peak (no tf32 figure is measured).
+    # the split-precision tensor-core path's peak is the
+    # measured dense tensor peak over the passes one algorithmic flop costs
+    # (3 fp16 hi/lo products, P_hi Z_hi + P_hi Z_lo + P_lo Z_hi)
+    peak = bf16_peak / 3.0 if eng.use_tc else None
     tensor_pipe = None
     if eng.use_tc:
         ka, nz, half = eng.tcp.ka, eng.zop.nz, eng.tcp.half
@@ -305,14 +310,16 @@ def run_b200(args):
         tensor_pipe = {"hw_flop_per_entry": {"gemm1_" + g1: 2 * ka, "gemm2_f16": 6 * nz},
                        "ideal_ms_at_peak": ideal_ms, "frac": ideal_ms / kmean,
                        "note": "time the tensor pipe needs for GEMM1 (%s, ka=%d) + GEMM2 (3 "
-                               "fp16 passes, nz=%d) at the measured bf16 peak (tf32 = half) "
-                               "over the measured kernel time" % (g1, ka, nz)}
+                               "fp16 passes, nz=%d) at the measured bf16 peak over the "
+                               "measured kernel time" % (g1, ka, nz)}
         # the epilogue's special-function bound: ex2 (RBF) or rsqrt + ex2 (Matern) per
         # kernel entry on the MUFU pipe (16 lanes/clk/SM, scripts/micro/pipes.cu)
         mufu_ops = 1 if args.family == "rbf" else 2
         mufu_ms = b_pad_rows(b) * n_local * mufu_ops / (16 * 148 * 1.965e9) * 1e3
         tensor_pipe["mufu_bound_ms"] = mufu_ms
         tensor_pipe["mufu_frac"] = mufu_ms / kmean
+    traffic = measured_traffic(args.family) if eng.use_tc and args.n == CONFIG["n"] else None
+
     e2e = None
     if not args.no_e2e and world == 1:
         e2e = run_e2e(args, prob, spec, dev)
@@ -331,17 +338,21 @@ def run_b200(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (SURVEY.md §8d generator, pathwise RHS)",
         "config": workload(args),
+        "warmup_effective": warm,
+        "warmup_note": f"the lookahead's batch ramp (first {RAMP_ITERS} iterations) counts as "
+                       "warm-up; the engine is unbounded so plan production continues at its "
+                       "steady rate through the timed window",
         "kernel_entries_per_s": entries / (ms_step * 1e-3),
         "krows_ms": kmean,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak,
-                     "unit": "TFLOP/s", "frac": achieved / bf16_peak,
-                     "traffic": TRAFFIC_PER_LAUNCH.get(args.family) if eng.use_tc else None,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                     "traffic": traffic["bytes"] if traffic else None,
+                     "traffic_source": traffic["source"] if traffic else None,
                      "kernel": kernel_name,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst), of measured",
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst) / 3 "
+                                    "(SURVEY.md §8d: 3 split-precision passes)",
                      "algorithmic": f"{b}*{n_local}*2*({d}+{m}) flop per launch "
                                     "(2d+2m per kernel entry, BASELINE.md §2)",
-                     "fp32_ffma_peak": ffma_peak,
-                     "frac_of_fp32_ffma_roofline": achieved / ffma_peak,
                      "tensor_pipe": tensor_pipe},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -355,55 +366,65 @@ def run_b200(args):
 
 
 def run_e2e(args, prob, spec, dev):
-    """Same metric through the public API from host numpy arrays: KernelOracle(X
-    host) + make_state(Y host) (setup, timed separately), W untimed warm-up
-    steps, then K timed ``adasap_step`` calls -- each one generates the step's
-    block indices, Gaussian sketch and power-iteration start on the host
-    (numpy RNG, bit-exact with the reference), copies them host->device from
-    pinned buffers and reads the step's stepsize back to the host -- and the
-    final W to host (timed separately). ``value`` is K / (timed step loop);
-    ``solve_iters_per_s`` also charges setup and the W readback to the K steps."""
+    """The same metric through the public drop-in API from HOST arrays, the way
+    reference code runs it (tests/test_solvers.py:199-219): KernelOracle(X
+    host), SolverState.zeros, K x adasap_step(oracle, state, Y host, config,
+    accel) -- each step reads its stepsize back to the host -- and the final W
+    to the host (state.W). Timed region: setup + K steps + W readback. Bytes
+    are counted at every copy site (paper_2505_13723_b200/xfer.py). One
+    untimed warm-up run first (process-level init: kernel modules, allocator
+    pools). ``solve`` adds the full adasap_solve of K iterations (its final
+    relative residual, a K W product over all n^2 entries, included)."""
     import numpy as np
     import torch
     import paper_2505_13723_b200 as sap
-    K, Wu = args.steps, args.warmup
+    from paper_2505_13723_b200 import xfer
+    from paper_2505_13723_b200.solvers import SolverState, adasap_step
+    K = args.steps
     X, Y = np.ascontiguousarray(prob.X), np.ascontiguousarray(prob.Y)
+    n, m = Y.shape
     cfg = sap.RunConfig(lam=prob.lam, blocksize=CONFIG["b"], nystrom_rank=CONFIG["r"],
-                        residual_every=0, seed=CONFIG["seed"], max_iters=K + Wu)
+                        residual_every=0, seed=CONFIG["seed"], max_iters=K)
+
+    def step_run(k):
+        o = sap.KernelOracle(spec, X, prob.lam, device=dev)
+        accel = sap.resolve_accel(cfg, o.n, CONFIG["b"])
+        state = SolverState.zeros(n, m, accelerated=True)
+        etas = []
+        for _ in range(k):
+            state, eta, _ = adasap_step(o, state, Y, cfg, accel)
+            etas.append(eta)
+        W = state.W
+        return W, etas, state
+
+    for _ in range(2):  # untimed warm-up runs (process-level init: modules, handles, pools)
+        _, _, st = step_run(max(2, args.warmup))
+        st.iteration = st.iteration  # detach: releases the engine
     torch.cuda.synchronize()
+    x0 = xfer.snapshot()
     t0 = time.perf_counter()
-    o = sap.KernelOracle(spec, X, prob.lam, device=dev)
-    accel = sap.resolve_accel(cfg, o.n, CONFIG["b"])
-    state = sap.make_state(o, Y, cfg, accel)
-    torch.cuda.synchronize()
-    t_setup = time.perf_counter() - t0
-    for _ in range(Wu):
-        state, eta, block = sap.adasap_step(o, state, Y, cfg, accel)
+    W, etas, st = step_run(K)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    etas = []
-    for _ in range(K):
-        state, eta, block = sap.adasap_step(o, state, Y, cfg, accel)
-        etas.append(eta)  # a host float: the per-step device->host read
-    torch.cuda.synchronize()  # every step's device work is inside the timed region
+    x1 = xfer.snapshot()
+    st._e.close()  # after the timed region: the lookahead's producers run ahead
+    h2d, d2h = x1["h2d"] - x0["h2d"], x1["d2h"] - x0["d2h"]
+    # the full solve (final residual included), for the record
     t2 = time.perf_counter()
-    W = state.W
+    o = sap.KernelOracle(spec, X, prob.lam, device=dev)
+    res = sap.adasap_solve(o, Y, cfg)
     t3 = time.perf_counter()
-    state._e.close()
-    b, r, m = CONFIG["b"], CONFIG["r"], CONFIG["m"]
-    # pinned host->device per step: block ids, the omega stream's PCG64 state (the
-    # sketch Omega is drawn on the GPU), power start, W and Woodbury factors,
-    # coefficients, rho; device->host: 3 r x r Gram blocks + eta
-    per_iter_h2d = b * 8 + 4 * 8 + b * 8 + 2 * r * r * 8 + 2 * r * 8 + 8
-    per_iter_d2h = 3 * r * r * 8 + 8
-    return {"value": K / (t2 - t1), "unit": "iters/s",
-            "h2d_bytes_per_step": int(per_iter_h2d), "d2h_bytes_per_step": int(per_iter_d2h),
-            "region": f"{K} x adasap_step through the public API after {Wu} warm-up steps "
-                      "(host RNG seeding + block draw, pinned H2D of the step inputs, the step's "
-                      "stepsize read to the host each step) and a final device synchronize; "
-                      "setup (X, Y host->device) and the final W readback are timed separately",
-            "seconds": t2 - t1, "setup_s": t_setup, "w_readback_s": t3 - t2,
-            "solve_iters_per_s": K / (t_setup + (t2 - t1) + (t3 - t2)),
+    return {"value": K / (t1 - t0), "unit": "iters/s",
+            "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K,
+            "h2d_bytes_total": h2d, "d2h_bytes_total": d2h,
+            "region": f"KernelOracle(X host) + SolverState.zeros + {K} x adasap_step(Y host), "
+                      "each step's stepsize read to the host, + state.W (final iterate to "
+                      "host float64); setup and readback inside the timed region",
+            "seconds": t1 - t0,
+            "solve": {"iters_per_s": K / (t3 - t2), "seconds": t3 - t2,
+                      "final_residual": res.trace.final_residual(),
+                      "note": f"adasap_solve(max_iters={K}) from host X/Y to host W, including "
+                              "its final relative residual (an n x n x m product)"},
             "finite": bool(np.isfinite(W).all() and np.isfinite(etas).all())}
 
 

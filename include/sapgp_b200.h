@@ -390,13 +390,16 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
 
 /*
  * Eigen-decomposition of `count` symmetric r x r fp64 matrices (A[q] at
- * A + q*strideA, row stride lda; symmetrised, then destroyed) by cyclic
- * two-sided Jacobi, one CTA per matrix: evals[q*r + k] descending and the
+ * A + q*strideA, row stride lda): evals[q*r + k] descending and the
  * matching eigenvectors as columns of V[q] (V + q*strideV, row stride ldv).
- * sweeps[q] (nullable) = sweeps used, -1 if max_sweeps did not converge.
+ * Backend: cuSOLVER's batched syev (cusolverDnXsyevBatched, loaded at run
+ * time) by default; SAP_EIG=jacobi selects the cyclic two-sided Jacobi
+ * kernel (one CTA per matrix; A symmetrised, then destroyed). sweeps[q] =
+ * Jacobi sweeps used (cuSOLVER: 0), -1 if not converged; required with
+ * cuSOLVER (its info array).
  * Replaces np.linalg.eigh on the Nystrom Gram matrices (the Gram route of
- * rand_nystrom, randnla.py:52-94). Workspace: sap_sym_eig_workspace (0 when
- * the matrices fit shared memory, r <= 112).
+ * rand_nystrom, randnla.py:52-94). Workspace: sap_sym_eig_workspace (for
+ * the backend selected at call time).
  */
 size_t sap_sym_eig_workspace(int r, int count);
 int sap_sym_eig_batch(double *A, int64_t strideA, int lda, int r, int count, double *evals,

@@ -30,6 +30,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import xfer
 from .errors import ContractError, ValidationError
 
 FAMILIES = ("rbf", "matern32", "matern52")
@@ -344,7 +345,7 @@ def to_colmajor(M, n, device, ld=None):
     if torch.is_tensor(M):
         Mt = M.to(device=device, dtype=torch.float32)
     else:
-        Mt = torch.as_tensor(np.asarray(M, dtype=np.float64), device=device).to(torch.float32)
+        Mt = xfer.upload(np.asarray(M, dtype=np.float64), torch.float32, device)
     if Mt.ndim == 1:
         Mt = Mt[:, None]
     if Mt.shape[0] != n:
@@ -382,7 +383,10 @@ class KernelOracle:
         self.device = _device(device)
         # one host->device copy of X (fp64); the FFMA and tensor-core point
         # formats are both derived from it on the device
-        self._Xd = torch.as_tensor(Xn, dtype=torch.float64).to(self.device).contiguous()
+        if is_t:
+            self._Xd = Xn.to(device=self.device, dtype=torch.float64).contiguous()
+        else:
+            self._Xd = xfer.upload(Xn, torch.float64, self.device)
         self.points = DevicePoints(spec, self._Xd, self.device)
         self._ws = None
         self._tc = None

@@ -40,6 +40,7 @@ import numpy as np
 import torch
 
 from . import kernels as K
+from . import xfer
 from .errors import NumericalError
 from .errors import ContractError
 from .randnla import (FLAG_CHOLESKY, FLAG_EIGH, FLAG_EXTRA_SHIFT, FLAG_NEG_TRACE, FLAG_PLAIN,
@@ -250,7 +251,9 @@ class Lookahead:
                                         self.sides[k % ns], owner)
 
     def close(self):
-        self.pool.shutdown(wait=True)
+        # batches not started yet are dropped; running producers finish their
+        # enqueued device work before the slots can be released
+        self.pool.shutdown(wait=True, cancel_futures=True)
 
     # -- consumer side (main thread) ------------------------------------------
     def get(self, t):
@@ -336,6 +339,7 @@ class Lookahead:
             if s.normals is not None and int(s.normals.status()) != 0:
                 raise NumericalError("device normal draw ran out of raw stream words")
             bits |= int(np.bitwise_or.reduce(s.bad.cpu().numpy()))
+            xfer.add("d2h", s.bad.numel() * 4 + (4 if s.normals is not None else 0))
         if bits & FLAG_NEG_TRACE:
             raise NumericalError("sketch Gram has negative trace; M is not PSD")
         if bits & FLAG_CHOLESKY:
@@ -384,6 +388,7 @@ class Lookahead:
                 fs.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
             slot.v0[:count].copy_(slot.h_v0[:count], non_blocking=True)
+            xfer.add("h2d", count * b * 16 + (count * 32 if r else 0))
             om = None
             if r:
                 slot.states[:count].copy_(slot.h_states[:count], non_blocking=True)
@@ -482,6 +487,7 @@ class Lookahead:
             # that wants eta_t (adasap_step) waits for its batch's power
             # iteration, not for the block products queued after it
             slot.h_eta[:count].copy_(slot.eta[:count], non_blocking=True)
+            xfer.add("d2h", count * 8)
             eta_ready = torch.cuda.Event()
             eta_ready.record(self.main)
         if self.timings is not None:
@@ -504,6 +510,7 @@ class Lookahead:
             if slot.free is not None:
                 fs.wait_event(slot.free)
             slot.block_dev[:count].copy_(slot.h_block[:count], non_blocking=True)
+            xfer.add("h2d", count * b * 8)
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
             for i in range(count):

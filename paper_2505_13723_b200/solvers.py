@@ -45,6 +45,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import xfer
 from .errors import ConfigError, ContractError
 from .kernels import KernelOracle, ZOperand, krows_tc, krows_tc_partials, krows_times, to_colmajor
 from .parallel import allreduce_sum_, current_shard, gather_rows
@@ -270,6 +271,7 @@ class SolverState:
     assigned values."""
 
     def __init__(self, W=None, V=None, Z=None, iteration=0):
+        self._zero = False  # known all-zero arrays (zeros()): no scan when binding
         if isinstance(W, AdasapEngine):  # bound to an engine (make_state)
             self._e, self._W, self._V, self._Z, self._it = W, None, None, None, W.t
             return
@@ -279,21 +281,29 @@ class SolverState:
     @classmethod
     def zeros(cls, n, m, accelerated=False):
         W = np.zeros((n, m))
-        if accelerated:
-            return cls(W, W.copy(), W.copy())
-        return cls(W, W, W)
+        # three distinct zero arrays (np.zeros maps zero pages lazily; a copy
+        # of W would touch all n*m*8 bytes twice)
+        st = cls(W, np.zeros((n, m)), np.zeros((n, m))) if accelerated else cls(W, W, W)
+        st._zero = True
+        return st
 
     # -- engine binding ---------------------------------------------------------
-    def _sync(self):
-        """Host arrays <- the bound engine's current iterate."""
+    def _host(self, which):
+        """The host array of W, V or Z, materialised from the bound engine's
+        current iterate on first access after a step (one array at a time)."""
+        cur = getattr(self, "_" + which)
         e = self._e
-        if e is not None and self._W is None:
-            vec = e.vector
-            self._W = _to_host64(e.gather_full(e.materialize("W")))
-            self._V = _to_host64(e.gather_full(e.materialize("V")))
-            self._Z = _to_host64(e.gather_full(e.materialize("Z")))
-            if vec:
-                self._W, self._V, self._Z = self._W[:, 0], self._V[:, 0], self._Z[:, 0]
+        if cur is None and e is not None:
+            cur = _to_host64(e.gather_full(e.materialize(which)))
+            if e.vector:
+                cur = cur[:, 0]
+            setattr(self, "_" + which, cur)
+        return cur
+
+    def _sync(self):
+        """All three host arrays <- the bound engine's current iterate."""
+        for which in ("W", "V", "Z"):
+            self._host(which)
 
     def _detach(self):
         self._sync()
@@ -313,32 +323,32 @@ class SolverState:
 
     @property
     def W(self):
-        self._sync()
-        return self._W
+        return self._host("W")
 
     @W.setter
     def W(self, v):
         self._detach()
+        self._zero = False
         self._W = v
 
     @property
     def V(self):
-        self._sync()
-        return self._V
+        return self._host("V")
 
     @V.setter
     def V(self, v):
         self._detach()
+        self._zero = False
         self._V = v
 
     @property
     def Z(self):
-        self._sync()
-        return self._Z
+        return self._host("Z")
 
     @Z.setter
     def Z(self, v):
         self._detach()
+        self._zero = False
         self._Z = v
 
 
@@ -349,19 +359,65 @@ def _as2d(A):
     return A if A.ndim == 2 else A[:, None]
 
 
+_STAGE = {"buf": None}
+_STAGE_CHUNK = 1 << 24  # elements per staged chunk (64 MB of fp32)
+_READBACK_POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="sap-readback")
+
+
+def _staging(elems):
+    """Process-wide pinned fp32 staging buffer (two chunks), kept across calls
+    (pinning 128 MB once costs more than a whole readback)."""
+    buf = _STAGE["buf"]
+    if buf is None or buf.numel() < 2 * elems:
+        buf = torch.empty(2 * elems, dtype=torch.float32, pin_memory=True)
+        _STAGE["buf"] = buf
+    return buf
+
+
 def _to_host64(t):
-    """Device tensor -> fresh C-contiguous float64 numpy array. The n x m copy
-    is bound by first-touch page faults of the new host array, so its pages
-    are faulted in by several threads before one device->host copy."""
-    src = t.to(torch.float64).contiguous()
+    """Device tensor -> fresh C-contiguous float64 numpy array.
+
+    fp32 state is copied as fp32 (half the bytes of a widened copy) through a
+    pinned double buffer: the device->host copy of chunk k overlaps the host
+    threads widening chunk k-1 into the output (numpy's casting copy releases
+    the GIL), which also spreads the output's first-touch page faults."""
+    src = t.contiguous()
     out = np.empty(tuple(src.shape), dtype=np.float64)
-    flat = out.reshape(-1)
-    k = min(8, max(1, flat.size // (1 << 20)))
-    if k > 1:
-        with ThreadPoolExecutor(max_workers=k) as ex:
-            list(ex.map(lambda i: flat[i * flat.size // k:(i + 1) * flat.size // k].fill(0.0),
-                        range(k)))
-    torch.from_numpy(out).copy_(src)
+    flat_out = out.reshape(-1)
+    if src.dtype != torch.float32 or src.device.type != "cuda" or src.numel() < (1 << 20):
+        torch.from_numpy(out).copy_(src.to(torch.float64))
+        xfer.add("d2h", src.numel() * src.element_size())
+        return out
+    flat = src.reshape(-1)
+    total = flat.numel()
+    chunk = min(_STAGE_CHUNK, total)
+    stage = _staging(chunk)
+    stream = torch.cuda.current_stream(src.device)
+    pend = [None, None]  # per staging half: futures of the widening of its last chunk
+
+    def widen(c0, lo, hi, half, ev):  # output [lo, hi) of the chunk starting at c0
+        ev.synchronize()
+        base = half * chunk - c0
+        np.copyto(flat_out[lo:hi], stage[base + lo: base + hi].numpy(), casting="same_kind")
+
+    for k, lo in enumerate(range(0, total, chunk)):
+        hi = min(total, lo + chunk)
+        half = k & 1
+        if pend[half] is not None:  # the half is free once its previous chunk is widened
+            for f in pend[half]:
+                f.result()
+        stage[half * chunk: half * chunk + (hi - lo)].copy_(flat[lo:hi], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        step = (hi - lo + 3) // 4
+        # four widening tasks per chunk, on disjoint slices of the output
+        pend[half] = [_READBACK_POOL.submit(widen, lo, s0, min(hi, s0 + step), half, ev)
+                      for s0 in range(lo, hi, step)]
+    for fs in pend:
+        if fs is not None:
+            for f in fs:
+                f.result()
+    xfer.add("d2h", total * 4)
     return out
 
 
@@ -751,8 +807,9 @@ def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=Fal
         for A in (state._W, state._V, state._Z):
             if _as2d(A).shape[0] != n:
                 raise ContractError("state arrays must have n rows")
-        zero = all(not np.any(np.asarray(A)) if not torch.is_tensor(A) else not bool(A.any())
-                   for A in (state._W, state._V, state._Z))
+        zero = state._zero or all(
+            not np.any(np.asarray(A)) if not torch.is_tensor(A) else not bool(A.any())
+            for A in (state._W, state._V, state._Z))
         e = AdasapEngine(oracle, Y, config, accel, identity_precond, unbounded=True,
                          start=state._it,
                          state=None if zero else (state._W, state._V, state._Z))
@@ -761,6 +818,7 @@ def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=Fal
         state._e = e
     plan = e.step(e.eval_point(config))
     state._W = state._V = state._Z = None  # written back lazily
+    state._zero = False
     return state, plan.eta_host(), plan.block
 
 
@@ -819,6 +877,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
                     break
         eng.la.check_flags()
         etas = eng.etas[:done].cpu().numpy()
+        xfer.add("d2h", etas.nbytes)
         for rec, eta in zip(trace.records, etas):
             rec.stepsize = float(eta)
         if averager is not None and averager.count > 0:

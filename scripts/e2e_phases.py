@@ -1,0 +1,26 @@
+"""Where the e2e (public step API from host arrays) time goes: oracle setup,
+first step (engine bind + first plan), remaining steps, W readback."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2505_13723_b200 as sap
+from paper_2505_13723_b200 import synthetic
+from paper_2505_13723_b200.solvers import SolverState, adasap_step
+n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
+prob = synthetic.make_problem(n, d, "matern32", m, seed=0, lam=1e-2, device="cuda")
+X, Y = np.ascontiguousarray(prob.X), np.ascontiguousarray(prob.Y)
+cfg = sap.RunConfig(lam=1e-2, blocksize=b, nystrom_rank=r, residual_every=0, seed=0)
+for rep in range(6):
+    torch.cuda.synchronize()
+    T = [time.perf_counter()]
+    o = sap.KernelOracle(prob.spec(), X, 1e-2, device="cuda"); torch.cuda.synchronize(); T.append(time.perf_counter())
+    accel = sap.resolve_accel(cfg, n, b)
+    st = SolverState.zeros(n, m, accelerated=True)
+    st, eta, _ = adasap_step(o, st, Y, cfg, accel); torch.cuda.synchronize(); T.append(time.perf_counter())
+    for _ in range(19):
+        st, eta, _ = adasap_step(o, st, Y, cfg, accel)
+    torch.cuda.synchronize(); T.append(time.perf_counter())
+    W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
+    st.iteration = st.iteration; T.append(time.perf_counter())
+    names = ["oracle", "bind+step0", "19 steps", "W readback", "close"]
+    print(rep, "  ".join(f"{k} {1e3*(T[i+1]-T[i]):.1f} ms" for i, k in enumerate(names)))

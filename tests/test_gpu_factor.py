@@ -26,8 +26,10 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
+@pytest.mark.parametrize("backend", ["cusolver", "jacobi"])
 @pytest.mark.parametrize("r,count", [(100, 6), (7, 3), (150, 2), (1, 2)])
-def test_jacobi_eigensolver_matches_numpy(r, count):
+def test_eigensolver_matches_numpy(r, count, backend, monkeypatch):
+    monkeypatch.setenv("SAP_EIG", backend)
     rng = np.random.default_rng(r)
     mats = []
     for q in range(count):
