@@ -147,7 +147,7 @@ class TcPoints:
     for every point (rows are gathered per block) and column form CA for the
     points of one shard [lo, hi)."""
 
-    def __init__(self, spec, X, device, lo=0, hi=None):
+    def __init__(self, spec, X, device, lo=0, hi=None, with_rows=True):
         Xd = torch.as_tensor(np.asarray(X, dtype=np.float64) if not torch.is_tensor(X) else X,
                              dtype=torch.float64).to(device).contiguous()
         n, d = Xd.shape
@@ -158,11 +158,15 @@ class TcPoints:
             raise ContractError(f"tensor-core path supports d <= 19 (got d={d})")
         inv = torch.as_tensor(np.broadcast_to(1.0 / spec.lengthscales, (d,)).copy(), device=device)
         self._ls, self._family = spec.lengthscales, spec.family
-        self.RA = torch.empty((max(n, 1), self.ka), dtype=torch.float32, device=device)
+        # with_rows=False: column features of [lo, hi) only (a shard's columns
+        # for a one-off product); gather_rows is then unavailable
+        self.RA = torch.empty((max(n, 1) if with_rows else 1, self.ka), dtype=torch.float32,
+                              device=device)
         self.CA = torch.empty((max(hi - lo, 1), self.ka), dtype=torch.float32, device=device)
         with torch.cuda.device(device):
-            nat.call("sap_tc_points", nat.ptr(Xd), n, d, nat.ptr(inv), spec.code, self.ka,
-                     nat.ptr(self.RA), None, nat.stream_handle())
+            if with_rows:
+                nat.call("sap_tc_points", nat.ptr(Xd), n, d, nat.ptr(inv), spec.code, self.ka,
+                         nat.ptr(self.RA), None, nat.stream_handle())
             if hi > lo:
                 nat.call("sap_tc_points", nat.ptr(Xd[lo:hi]), hi - lo, d, nat.ptr(inv), spec.code,
                          self.ka, None, nat.ptr(self.CA), nat.stream_handle())
@@ -496,6 +500,14 @@ class KernelOracle:
         """k(Xstar, X) @ W -- external rows, no diagonal rule (kernels.py:161-176)."""
         vector = (W.ndim == 1)
         like_np = not torch.is_tensor(W)
+        from .parallel import allreduce_sum_, current_shard
+        sh = current_shard(self.n)
+        if torch.is_tensor(W) and W.is_cuda and sh.world > 1 and W.shape[0] == sh.size \
+                and sh.size != self.n:
+            # W is this rank's shard (a device-resident solve, solvers.py): the
+            # partial k(X*, X_shard) W_shard, summed over ranks (one t x m
+            # all-reduce, SURVEY.md §8e) -- no n x m gather
+            return self._cross_matmul_shard(Xstar, W, sh, vector, allreduce_sum_)
         if W.shape[0] != self.n:
             raise ContractError("W must have n rows")
         star = DevicePoints(self.spec, Xstar, self.device)
@@ -524,6 +536,65 @@ class KernelOracle:
         krows_times(self.spec, self.points, star.Xs, star.sqn, None, Rcm, out,
                     ws=self._workspace(t, m, self.n))
         return _finish(out, like_np, vector)
+
+    def star_rows(self, Xstar, m):
+        """Row operands of external points: ("tc", features) or ("pts", Xs, sqn)."""
+        star = DevicePoints(self.spec, Xstar, self.device)
+        if star.d != self.d:
+            raise ContractError("point dimension does not match the training inputs")
+        t = star.n
+        if self.use_tc(m) and t >= 16 and self.tc_points(*self._tc_range()).fits_half(Xstar):
+            tcp = self._tc
+            Xs64 = torch.as_tensor(np.asarray(Xstar, dtype=np.float64) if not torch.is_tensor(
+                Xstar) else Xstar, dtype=torch.float64).to(self.device).contiguous()
+            RAs = torch.zeros(((t + 255) // 256 * 256, tcp.ka), dtype=torch.float32,
+                              device=self.device)
+            inv = torch.as_tensor(np.broadcast_to(1.0 / self.spec.lengthscales,
+                                                  (self.d,)).copy(), device=self.device)
+            nat.call("sap_tc_points", nat.ptr(Xs64), t, self.d, nat.ptr(inv), self.spec.code,
+                     tcp.ka, nat.ptr(RAs), None, nat.stream_handle())
+            return ("tc", RAs.to(tcp.dtype)), t
+        return ("pts", star.Xs, star.sqn), t
+
+    def _tc_range(self):
+        return (self._tc.lo, self._tc.hi) if self._tc is not None else (0, self.n)
+
+    def _cross_matmul_shard(self, Xstar, W_local, sh, vector, allreduce):
+        Wl = W_local[:, None] if W_local.ndim == 1 else W_local
+        m = Wl.shape[1]
+        Wcm = to_colmajor(Wl, sh.size, self.device)
+        rows, t = self.star_rows(Xstar, m)
+        out = torch.empty((t, m), dtype=torch.float32, device=self.device)
+        tcp = self._tc if self._tc is not None and (self._tc.lo, self._tc.hi) == (sh.lo, sh.hi) \
+            else None
+        range_product(self, rows, None, Wcm, sh.lo, sh.hi, out, tcp=tcp)
+        allreduce(out)
+        return out[:, 0] if vector else out
+
+
+def range_product(oracle, rows, row_ids, Wcm, lo, hi, out, accumulate=False, tcp=None):
+    """out (nrows x m fp32) (+)= variance * K(rows, X[lo:hi]) @ W[lo:hi]: the
+    block-row kernel over one contiguous range of column points (a shard).
+
+    ``rows``: ("tc", RAg) tensor-core row features (nrows padded to 256) or
+    ("pts", Rs, rsq) prepared FFMA rows; ``Wcm`` column-major (m x >= hi-lo)
+    fp32; ``row_ids`` global ids of the rows (diagonal rule) or None.
+    ``tcp``: the TcPoints of [lo, hi) if the caller holds them; otherwise the
+    column features are built for the call and not cached in the oracle."""
+    nrows = out.shape[0]
+    m = Wcm.shape[0]
+    if hi <= lo:
+        if not accumulate:
+            out.zero_()
+        return out
+    if rows[0] == "tc":
+        if tcp is None or (tcp.lo, tcp.hi) != (lo, hi):
+            tcp = TcPoints(oracle.spec, oracle._Xd, oracle.device, lo, hi, with_rows=False)
+        zop = ZOperand(m, hi - lo, oracle.device).fill(Wcm)
+        return krows_tc(oracle.spec, tcp, rows[1], nrows, row_ids, zop, out,
+                        accumulate=accumulate)
+    return krows_times(oracle.spec, oracle.points, rows[1], rows[2], row_ids, Wcm, out,
+                       col_base=lo, accumulate=accumulate, ncols=hi - lo, col_offset=lo)
 
 
 def kernel_eval(spec, x, y):

@@ -175,9 +175,20 @@ class TailAverager:
         self.count = 0
 
     def add(self, index, iterate):
-        if self.start <= index <= self.stop:
-            self._sum = iterate.clone() if self._sum is None else self._sum + iterate
-            self.count += 1
+        """Accumulate in float64, in place (numpy iterates as in the reference,
+        or device tensors: one preallocated fp64 accumulator, no per-add copy)."""
+        if not self.start <= index <= self.stop:
+            return
+        if torch.is_tensor(iterate):
+            if self._sum is None:
+                self._sum = torch.zeros(iterate.shape, dtype=torch.float64, device=iterate.device)
+            self._sum.add_(iterate.to(torch.float64))
+        else:
+            it = np.asarray(iterate, dtype=np.float64)
+            if self._sum is None:
+                self._sum = np.zeros(it.shape)
+            self._sum += it
+        self.count += 1
 
     def average(self):
         if self.count == 0:
@@ -440,9 +451,15 @@ class AdasapEngine:
         self.shard = shard if shard is not None else current_shard(n)
         Ya = Y if torch.is_tensor(Y) else np.asarray(Y, dtype=np.float64)
         self.vector = Ya.ndim == 1
-        if Ya.shape[0] != n:
+        sh0 = self.shard
+        # a CUDA tensor with exactly this shard's rows is taken as the local
+        # part of a device-resident right-hand side (no full-n copy per rank)
+        local_y = torch.is_tensor(Ya) and Ya.is_cuda and sh0.world > 1 and \
+            Ya.shape[0] == sh0.size and sh0.size != n
+        self.local_y = local_y
+        if Ya.shape[0] != n and not local_y:
             raise ContractError("right-hand side must have n rows")
-        Yl = Ya[self.shard.lo:self.shard.hi]
+        Yl = Ya if local_y else Ya[self.shard.lo:self.shard.hi]
         if Yl.ndim == 1:
             Yl = Yl[:, None]
         self.m = int(Ya.shape[1]) if Ya.ndim == 2 else 1
@@ -752,18 +769,50 @@ class AdasapEngine:
         """Concatenate shards (n x m) on every rank."""
         return gather_rows(local, self.n, self.shard)
 
+    def y_norm(self):
+        """||Y||_F over all ranks from the device-resident right-hand sides."""
+        part = (self.Y[:, :self.shard.size].double() ** 2).sum().reshape(1)
+        allreduce_sum_(part)
+        return max(float(torch.sqrt(part)), np.finfo(np.float64).tiny)
+
     def relative_residual(self, W_local, ynorm):
-        """||K W + lam W - Y||_F / ||Y||_F over this shard's rows, summed over ranks
-        (solvers.py:254-257)."""
-        Wfull = self.gather_full(W_local)
-        Wcm = Wfull.T.contiguous()
+        """||K W + lam W - Y||_F / ||Y||_F (solvers.py:254-257), shard-local:
+        rank r forms (K W)[shard r] = sum_q K[shard r, shard q] W_q, the shards
+        W_q arriving one at a time by broadcast (so no rank holds more than
+        two n/P x m shards; no n x m all-gather), then one scalar all-reduce."""
+        import torch.distributed as tdist
+        from .kernels import range_product
+        from .dist import partition
         sh = self.shard
+        m = self.m
+        Wcm = torch.zeros((m, self.ld), dtype=torch.float32, device=self.dev)
+        if sh.size:
+            Wcm[:, :sh.size] = W_local.T
         if sh.size == 0:
             part = torch.zeros(1, dtype=torch.float64, device=self.dev)
+            KW = None
         else:
-            # rows of this shard against all points: the same fused product (K5)
             ids = torch.arange(sh.lo, sh.hi, device=self.dev, dtype=torch.int64)
-            KW = self.o.rows_times_device(ids, Wcm)
+            if self.use_tc:
+                rows = ("tc", self.tcp.gather_rows(ids))
+            else:
+                rows = ("pts",) + self.o.points.gather(ids)
+            KW = torch.empty((sh.size, m), dtype=torch.float32, device=self.dev)
+        ranges = [(0, self.n)] if sh.world == 1 else (
+            partition(self.n, sh.world) if self.n >= sh.world else
+            [(0, self.n) if q == 0 else (self.n, self.n) for q in range(sh.world)])
+        for q, (lo, hi) in enumerate(ranges):
+            if sh.world > 1:
+                ldq = max(4, (hi - lo + 3) // 4 * 4)
+                buf = Wcm if q == sh.rank else torch.empty((m, ldq), dtype=torch.float32,
+                                                           device=self.dev)
+                tdist.broadcast(buf, src=q)
+            else:
+                buf = Wcm
+            if KW is not None:
+                range_product(self.o, rows, ids, buf, lo, hi, KW, accumulate=q > 0,
+                              tcp=self.tcp if q == sh.rank else None)
+        if KW is not None:
             res = KW.double() + self.lam * W_local.double() - self.Y[:, :sh.size].T.double()
             part = (res * res).sum().reshape(1)
         allreduce_sum_(part)
@@ -846,8 +895,11 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
         accel = resolve_accel(config, n, b)
     total = budget_iterations(config, b / n)
     eng = AdasapEngine(oracle, Y, config, accel, identity_precond, total)
+    # a CUDA right-hand side keeps the solve on the device: W is returned as
+    # this rank's shard (fp32 CUDA tensor), never gathered to n x m
+    device_out = torch.is_tensor(Y) and Y.is_cuda
     try:
-        ynorm = _y_norm(Y)
+        ynorm = eng.y_norm() if device_out else _y_norm(Y)
         trace = ConvergenceTrace()
         averager = TailAverager(total, (n, eng.m)) if config.tail_average else None
         diverged = False
@@ -884,7 +936,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
             W_loc = averager.average()
         else:
             W_loc = eng.materialize("W")
-        W = _to_host64(eng.gather_full(W_loc))
+        W = W_loc if device_out else _to_host64(eng.gather_full(W_loc))
     finally:
         eng.close()
     return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)

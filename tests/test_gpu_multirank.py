@@ -3,7 +3,10 @@ share the one GPU of the test box and each solves on its half of the point dimen
 (sharded block product, one all-reduce of the b x m gradient per iteration,
 owner-rank production of the lookahead batches); the trajectory must equal
 the single-process one: identical blocks, stepsizes and residual trace to
-fp32 accuracy, W to 1e-4 (fp32 sums in a different shard order)."""
+fp32 accuracy, W to 1e-4 (fp32 sums in a different shard order). The
+residual is the shard-local ring (no n x m all-gather), and a device-resident
+solve (per-rank rows of Y as a CUDA tensor, W kept as shards) predicts by the
+sharded cross product with one t x m all-reduce."""
 import os
 import subprocess
 import sys
@@ -38,3 +41,8 @@ def test_ranks_match_one(tmp_path, ranks):
     due = ~np.isnan(one["res"])
     np.testing.assert_allclose(two["res"][due], one["res"][due], rtol=1e-4)
     assert np.abs(two["W"] - one["W"]).max() / np.abs(one["W"]).max() < 1e-4
+    # the shard-local residual ring and the device-resident solve + sharded
+    # prediction agree with the single-process run
+    np.testing.assert_allclose(two["res_d"][due], one["res"][due], rtol=1e-4)
+    for k in ("pred_d", "pred_h"):
+        assert np.abs(two[k] - one["pred_h"]).max() / np.abs(one["pred_h"]).max() < 1e-4
