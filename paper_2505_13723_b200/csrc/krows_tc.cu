@@ -2,6 +2,7 @@
 // kernel itself is in krows_tc.cuh, instantiated per family in krows_tc_*.cu).
 #include <cstdio>
 #include <cstdarg>
+#include <atomic>
 #include <mutex>
 #include <cstdlib>
 
@@ -404,8 +405,12 @@ bool use_pair(int nz, int ka) {
 size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols) {
   const int64_t t1 = (ncols + NT - 1) / NT, t2 = (ncols + tck2::NT - 1) / tck2::NT;
   const int64_t s = std::max<int64_t>(tc_splits(b, t1), tc2_splits(b, t2));
-  return size_t(s) * size_t(b) * size_t(m) * sizeof(float);
+  // partial sums, then (256-byte aligned) the dynamic unit counter
+  return (size_t(s) * size_t(b) * size_t(m) * sizeof(float) + 255) / 256 * 256 + 256;
 }
+
+// launch tags of the dynamic unit counter (any start value works)
+std::atomic<unsigned> g_tc_epoch{0x5a17u};
 
 int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
                       const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
@@ -454,6 +459,14 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
   if (!ws || ws_bytes < need)
     return fail(SAP_ERR_CONTRACT, "krows_tc: workspace %zu < %zu bytes", ws_bytes, need);
   p.part = static_cast<float *>(ws);
+  {
+    const size_t part_bytes = (need + 255) / 256 * 256;
+    const char *st_env = getenv("SAP_TC_STATIC");
+    if (ws_bytes >= part_bytes + 8 && !(st_env && atoi(st_env))) {
+      p.sched = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + part_bytes);
+      p.epoch = g_tc_epoch.fetch_add(1u, std::memory_order_relaxed);
+    }
+  }
   // the next operand inside the CTA-pair kernel (16-byte vector rows only)
   auto al16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   const bool side = Zhi_next && pair && ldp % 4 == 0 && ldz % 8 == 0 && al16(P) &&

@@ -98,6 +98,10 @@ struct Params {
   int debug;               // profiling switches, 0 in production
   unsigned long long *prof;  // per-CTA role timers (SAP_TC_DEBUG=9), else NULL
   zop::Next zn;            // next iterate's operand (CTA-pair kernel side job; Zhi NULL: none)
+  unsigned long long *sched;  // dynamic unit counter (CTA-pair kernel): high word = the launch's
+                              // epoch, low word = units taken; NULL: static round-robin units
+  unsigned epoch;             // this launch's tag (a counter left by another launch, or any
+                              // stale value, is re-armed by the first fetch)
 };
 
 template <int NZ, int KA>

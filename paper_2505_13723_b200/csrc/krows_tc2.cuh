@@ -65,6 +65,10 @@ constexpr int NB = 3;       // S/P tiles in flight in TMEM (columns 0..383)
 constexpr int kSeg = SAP_KSEG;  // tiles per TMEM accumulator segment (2048 points)
 constexpr uint32_t kGCol = NB * NT;  // the (single) accumulator, nz columns
 constexpr int kEpiGroups = 4;                       // epilogue warpgroups
+constexpr int kUR = 4;                              // unit ring entries (dynamic schedule)
+// readers of a unit id that release it: the peer's producer, the MMA issuer
+// and every epilogue warp of both CTAs
+constexpr int kUnitReaders = 1 + 1 + 2 * 4 * kEpiGroups;
 constexpr int kThreads = 128 * (1 + kEpiGroups);    // + the control warpgroup
 // setmaxnreg split of the registers the launch holds (640 threads x 96): the
 // increases can only draw what the control warpgroup's decrease released,
@@ -129,7 +133,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t *p_full = s_full + NB;         // [NB]      leader: 16 warp arrivals
   uint64_t *g_full = p_full + NB;         // [1]       both
   uint64_t *g_empty = g_full + 1;         // [1]       leader: 16 warp arrivals
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(g_empty + 1);
+  uint64_t *u_full = g_empty + 1;         // [kUR]     both: the leader producer's unit id
+  uint64_t *u_empty = u_full + kUR;       // [kUR]     leader: every consumer read it
+  int *u_ring = reinterpret_cast<int *>(u_empty + kUR);  // [kUR] unit ids (-1: done)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(u_ring + kUR);
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < STAGES; ++s) {
@@ -146,6 +153,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     tc::mbar_init(tc::smem_u32(g_full), 1);
     tc::mbar_init(tc::smem_u32(g_empty), 8 * kEpiGroups);
+    for (int k = 0; k < kUR; ++k) {
+      tc::mbar_init(tc::smem_u32(&u_full[k]), 1);
+      tc::mbar_init(tc::smem_u32(&u_empty[k]), kUnitReaders);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -164,6 +175,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   const int units = p.row_tiles * p.splits;  // row_tiles counts 256-row pair tiles here
+  // Units (256-row tile x column split) are handed out dynamically: the
+  // leader's producer takes the next one from a global counter and publishes
+  // it to every role of both CTAs through a small shared-memory ring, so a
+  // pair that starts late (SMs still held by a concurrent kernel on another
+  // stream) simply takes fewer units instead of stretching the launch. The
+  // partial sums are indexed by unit, so the result does not depend on which
+  // pair ran what. p.sched == NULL: static round-robin units.
+  const bool dyn = p.sched != nullptr;
+  auto unit_at = [&](int k) -> int {  // static schedule
+    const int u = pair + k * npairs;
+    return u < units ? u : -1;
+  };
+  // consumer side of the ring: wait for entry k, read it, release it to the leader
+  auto take_unit = [&](int k, bool arrive) -> int {
+    if (!dyn) return unit_at(k);
+    const int slot = k % kUR;
+    tc::mbar_wait_acquire_cluster(tc::smem_u32(&u_full[slot]), (k / kUR) & 1);
+    const int u = *reinterpret_cast<volatile int *>(&u_ring[slot]);
+    if (arrive) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&u_empty[slot]), 0));
+    return u;
+  };
 
   if (warp < 4) tc::setmaxnreg_dec<kCtlRegs>();
   if (warp == 0) {
@@ -174,7 +206,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t full0 = tc::smem_u32(full), empty0 = tc::smem_u32(empty);
       const uint32_t stage0 = tc::smem_u32(sStage);
       unsigned long long tw = 0, ti = 0, c0;
-      for (int u = pair; u < units; u += npairs, ++uc) {
+      for (int k = 0;; ++k, ++uc) {
+        int u;
+        if (dyn && cr == 0) {  // the leader's producer fetches and publishes
+          const int slot = k % kUR;
+          tc::mbar_wait(tc::smem_u32(&u_empty[slot]), ((k / kUR) & 1) ^ 1);
+          // u = this launch's next unit: the counter is tagged with the launch's
+          // epoch, so no reset between launches is needed
+          unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(p.sched), prev;
+          do {
+            prev = old;
+            const bool mine = unsigned(old >> 32) == p.epoch;
+            const unsigned long long nxt =
+                (static_cast<unsigned long long>(p.epoch) << 32) | ((mine ? (old & 0xffffffffull) : 0ull) + 1ull);
+            u = mine ? int(old & 0xffffffffull) : 0;
+            old = atomicCAS(p.sched, prev, nxt);
+          } while (old != prev);
+          if (u >= units) u = -1;
+          u_ring[slot] = u;
+          tc::st_cluster_u32(tc::mapa(tc::smem_u32(&u_ring[slot]), 1), uint32_t(u));
+          tc::mbar_arrive_release_cluster(tc::mapa(tc::smem_u32(&u_full[slot]), 0));
+          tc::mbar_arrive_release_cluster(tc::mapa(tc::smem_u32(&u_full[slot]), 1));
+        } else {
+          u = take_unit(k, true);
+        }
+        if (u < 0) break;
         const int rt = u % p.row_tiles, split = u / p.row_tiles;
         int64_t t0, t1;
         split_range(p.tiles, p.splits, split, t0, t1);
@@ -230,7 +286,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t sc = 0;
       int uc = 0;
       unsigned long long wf = 0, wp = 0, wg = 0, i1 = 0, i2 = 0, cc;
-      for (int u = pair; u < units; u += npairs, ++uc) {
+      for (int k = 0;; ++k, ++uc) {
+        const int u = take_unit(k, true);
+        if (u < 0) break;
         const int split = u / p.row_tiles;
         int64_t t0, t1;
         split_range(p.tiles, p.splits, split, t0, t1);
@@ -383,7 +441,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
       }
     };
-    for (int u = pair; u < units; u += npairs) {
+    for (int k = 0;; ++k) {
+      const int u = take_unit(k, false);
+      if (dyn) {  // one arrival per warp
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&u_empty[k % kUR]), 0));
+      }
+      if (u < 0) break;
       const int rt = u % p.row_tiles, split = u / p.row_tiles;
       int64_t t0, t1;
       split_range(p.tiles, p.splits, split, t0, t1);
@@ -469,6 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::cluster_sync();  // the peer's TMEM/barriers stay live until both CTAs are done
   tc::fence_after();
+
   if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * 16 + 11] = prof_clock() - kstart;
   if (warp == 2) tc::tmem_dealloc_pair(tmem, 512);
 }
