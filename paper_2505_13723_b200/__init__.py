@@ -12,7 +12,7 @@ CUDA device every product raises ``WorkerError``.
 __version__ = "0.1.0"
 
 from .baselines import pcg_solve, sap_solve, sdd_solve  # noqa: F401
-from .config import RunConfig, apply_overrides, kernel_from_dict, load_config  # noqa: F401
+from .config import RunConfig, kernel_from_dict  # noqa: F401
 from .dist import WorkerPool, col_dist_matmul, row_dist_matmul  # noqa: F401
 from .errors import (  # noqa: F401
     ConfigError,

@@ -188,7 +188,12 @@ class Lookahead:
         # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
         # mostly padding and the FFMA sketch, ~4x more precise, costs little)
-        self.tc_sketch = tcp is not None and self.r and b >= 512 and oracle.use_tc(self.r)
+        # the sketch K[B,B] Omega: by default a batched fp32 GEMM against the
+        # K_BB tiles the power iteration needs anyway (SAP_SKETCH=tc: the
+        # block-row kernel with the block's own points as columns, round 1)
+        self.sketch_gemm = os.environ.get("SAP_SKETCH", "gemm") == "gemm"
+        self.tc_sketch = (not self.sketch_gemm and tcp is not None and self.r and b >= 512
+                          and oracle.use_tc(self.r))
         if self.tc_sketch:
             self.sk_pos = torch.arange(b, dtype=torch.int64, device=dev)
             need = K.nat.load().sap_krows_tc_workspace(b, self.r, b)
@@ -403,7 +408,14 @@ class Lookahead:
             pts.gather(flat, out=(slot.Xb[:count].view(-1, pts.ldx), slot.rsq[:count].view(-1)))
             if self.tcp is not None:
                 self.tcp.gather_rows_batch(bd, slot.RAg[:count])
-            if r:
+            if r and self.sketch_gemm:
+                # K_BB once per iteration (the power iteration's operand too),
+                # then the sketch K_BB Omega as one batched fp32 GEMM
+                # (row_dist_matmul, dist.py:130-147; 2 b^2 r flop per iteration)
+                K.ktile_f32_batch(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
+                                  slot.Kbb[:count])
+                torch.bmm(slot.Kbb[:count, :, :b], om.to(torch.float32), out=sketch)
+            elif r:
                 omc = om.transpose(1, 2).to(torch.float32).contiguous()  # (count, r, b) RHS
                 if self.tc_sketch:
                     # K[B,B] Omega on the tensor cores: the block's own points as
@@ -457,8 +469,9 @@ class Lookahead:
         tm3 = time.perf_counter()
         with torch.cuda.device(self.dev), torch.cuda.stream(side):
             side.wait_event(ev)  # phase 1 (fast stream) done: Xb, rsq, U, Mc, E, rho
-            K.ktile_f32_batch(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
-                              slot.Kbb[:count])
+            if not (r and self.sketch_gemm):
+                K.ktile_f32_batch(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
+                                  slot.Kbb[:count])
             inputs = torch.cuda.Event()
             inputs.record(side)
         # The power iteration is one long cluster kernel on 128 SMs: on the side

@@ -10,17 +10,23 @@ n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
 prob = synthetic.make_problem(n, d, "matern32", m, seed=0, lam=1e-2, device="cuda")
 X, Y = np.ascontiguousarray(prob.X), np.ascontiguousarray(prob.Y)
 cfg = sap.RunConfig(lam=1e-2, blocksize=b, nystrom_rank=r, residual_every=0, seed=0)
-for rep in range(6):
+for rep in range(8):
     torch.cuda.synchronize()
     T = [time.perf_counter()]
     o = sap.KernelOracle(prob.spec(), X, 1e-2, device="cuda"); torch.cuda.synchronize(); T.append(time.perf_counter())
     accel = sap.resolve_accel(cfg, n, b)
     st = SolverState.zeros(n, m, accelerated=True)
     st, eta, _ = adasap_step(o, st, Y, cfg, accel); torch.cuda.synchronize(); T.append(time.perf_counter())
-    for _ in range(19):
+    slow = []
+    for k in range(19):
+        h0 = time.perf_counter()
         st, eta, _ = adasap_step(o, st, Y, cfg, accel)
+        dt = time.perf_counter() - h0
+        if dt > 5e-3:
+            slow.append((k + 1, round(dt * 1e3, 1)))
     torch.cuda.synchronize(); T.append(time.perf_counter())
     W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
     st.iteration = st.iteration; T.append(time.perf_counter())
     names = ["oracle", "bind+step0", "19 steps", "W readback", "close"]
-    print(rep, "  ".join(f"{k} {1e3*(T[i+1]-T[i]):.1f} ms" for i, k in enumerate(names)))
+    print(rep, "  ".join(f"{k} {1e3*(T[i+1]-T[i]):.1f} ms" for i, k in enumerate(names)),
+          "slow steps (host ms):", slow, flush=True)

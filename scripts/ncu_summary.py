@@ -24,12 +24,18 @@ want = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "l1tex__m_xbar2l1tex_read_bytes.sum",
         "lts__t_bytes.sum", "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 print("== metrics")
+print("== kernel", vals[hdr.index("Kernel Name")][:100] if "Kernel Name" in hdr else "")
 for h, u, v in zip(hdr, units, vals):
     if h in want:
         print(f"  {h:70s} {v:>14s} {u}")
 src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
 H = src[1]
-D = src[2:]
+# a report with several kernels repeats the title/header rows: keep the first kernel's block
+D = []
+for r in src[2:]:
+    if r and (r[0] == "Kernel Name" or r[0] == H[0]):
+        break
+    D.append(r)
 ix = {k: H.index(k) for k in H}
 tot = sum(float(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in D)
 stalls = [k for k in H if k.startswith("stall_") and "Not Issued" not in k]

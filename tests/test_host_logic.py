@@ -25,8 +25,6 @@ def test_runconfig_defaults_and_validation():
         sap.RunConfig.from_dict({"lam": 1.0, "bogus": 1})
     with pytest.raises(sap.ConfigError):
         sap.RunConfig(blocksize=10).validate_for(5)
-    tree = sap.apply_overrides({}, ["run.lam=0.5", "run.tail_average=true", "kernel.family=rbf"])
-    assert tree == {"run": {"lam": 0.5, "tail_average": True}, "kernel": {"family": "rbf"}}
     spec = sap.kernel_from_dict({"family": "matern32", "lengthscales": 2.0}, d=3)
     assert spec.lengthscales.tolist() == [2.0, 2.0, 2.0]
 
