@@ -238,9 +238,62 @@ struct Handle {
 std::mutex g_pool_mu;
 std::vector<Handle *> g_pool;
 
+Handle *new_handle() {
+  Handle *th = new Handle;
+  Cusolver &c = cusolver();
+  if (c.ok && c.create(&th->h) == CUSOLVER_STATUS_SUCCESS) c.create_params(&th->p);
+  return th;
+}
+
+// The pool is filled once with warm handles: the first batched syev on a
+// fresh handle initialises for ~0.1 s, which inside the lookahead stalls the
+// solver; paying it up front (the first factorisation) keeps it out of steps.
+constexpr int kWarmHandles = 8;
+void prewarm_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    Cusolver &c = cusolver();
+    if (!c.ok) return;
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+    double *buf = nullptr;
+    int *info = nullptr;
+    void *dws = nullptr;
+    cudaMalloc(&buf, 64 * sizeof(double));
+    cudaMalloc(&info, sizeof(int));
+    const double eye[16] = {2, 0, 0, 0, 0, 3, 0, 0, 0, 0, 4, 0, 0, 0, 0, 5};
+    std::vector<Handle *> made;
+    for (int k = 0; k < kWarmHandles; ++k) {
+      Handle *th = new_handle();
+      made.push_back(th);
+      if (!th->h) continue;
+      size_t dw = 0, hw = 0;
+      if (c.bufsize(th->h, th->p, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, 4,
+                    CUDA_R_64F, buf, 4, CUDA_R_64F, buf + 16, CUDA_R_64F, &dw, &hw, 1) !=
+          CUSOLVER_STATUS_SUCCESS)
+        continue;
+      if (!dws) cudaMalloc(&dws, dw > 0 ? dw * 4 : 256);
+      th->host_ws.resize(hw);
+      cudaMemcpyAsync(buf, eye, sizeof(eye), cudaMemcpyHostToDevice, st);
+      c.set_stream(th->h, st);
+      c.syev(th->h, th->p, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, 4, CUDA_R_64F, buf,
+             4, CUDA_R_64F, buf + 16, CUDA_R_64F, dws, dw > 0 ? dw * 4 : 256,
+             th->host_ws.data(), hw, info, 1);
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(buf);
+    cudaFree(info);
+    cudaFree(dws);
+    cudaStreamDestroy(st);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (Handle *th : made) g_pool.push_back(th);
+  });
+}
+
 struct Lease {
   Handle *th = nullptr;
   Lease() {
+    prewarm_pool();
     {
       std::lock_guard<std::mutex> lk(g_pool_mu);
       if (!g_pool.empty()) {
@@ -248,11 +301,7 @@ struct Lease {
         g_pool.pop_back();
       }
     }
-    if (!th) {
-      th = new Handle;
-      Cusolver &c = cusolver();
-      if (c.ok && c.create(&th->h) == CUSOLVER_STATUS_SUCCESS) c.create_params(&th->p);
-    }
+    if (!th) th = new_handle();
   }
   ~Lease() {
     std::lock_guard<std::mutex> lk(g_pool_mu);

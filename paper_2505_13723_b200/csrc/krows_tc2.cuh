@@ -74,7 +74,10 @@ constexpr int kThreads = 128 * (1 + kEpiGroups);    // + the control warpgroup
 // increases can only draw what the control warpgroup's decrease released,
 // otherwise setmaxnreg.inc spins forever
 constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8;
-constexpr int kCtlRegs = 64;  // warps 2-3 stream the next operand (zop::next_pass)
+#ifndef SAP_CTL_REGS
+#define SAP_CTL_REGS 64
+#endif
+constexpr int kCtlRegs = SAP_CTL_REGS;  // warps 2-3 stream the next operand (zop::next_pass)
 constexpr int kEpiRegs = 104;
 static_assert(128 * kCtlRegs + 128 * kEpiGroups * kEpiRegs <= kThreads * kLaunchRegs,
               "setmaxnreg budget exceeds the launch allocation");

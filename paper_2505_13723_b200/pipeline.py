@@ -11,7 +11,7 @@ block-row product and the update depends only on (seed, t) and X:
     eta_t    = rand_power_stepsize(K[B,B] + lam I, (U, S), rho,
                                    10, substream(seed, "power", t)) :389-396
 
-so they are produced in batches by ``depth`` (default 4) host producer
+so they are produced in batches by ``depth`` (default 6) host producer
 threads, up to ``depth`` batches ahead of the block-row products that
 consume them; their GPU work is enqueued in order on the solver's stream
 (see Lookahead.__init__). Batch sizes ramp 1, 2, 4, ... up to
@@ -143,7 +143,11 @@ class Lookahead:
         # factorisation -- so two producers left the solver host-bound at ~1.43
         # ms per RBF iteration against 1.25 with four (scripts/host_bound.py,
         # config 3); SAP_LOOKAHEAD_DEPTH overrides
-        self.depth = max(2, int(os.environ.get("SAP_LOOKAHEAD_DEPTH", "4")))
+        # (round 2: with the factorisation on the device a producer no longer
+        # waits on the host; depth 6 keeps a fresh engine's ramp (batches of 1,
+        # 2, 4, ...) from stalling the first steps -- 19 steps after a bind in
+        # 30 ms instead of 42-390 ms at depth 4 -- at the same steady rate)
+        self.depth = max(2, int(os.environ.get("SAP_LOOKAHEAD_DEPTH", "6")))
         # depth + 1 slots of L fp32 b x b blocks: keep them under ~4 GB
         # slots: depth in production + the one being consumed + SAP_SPARE_SLOTS
         # (default 1): a batch's production first waits until its slot's
@@ -259,6 +263,12 @@ class Lookahead:
         # batches not started yet are dropped; running producers finish their
         # enqueued device work before the slots can be released
         self.pool.shutdown(wait=True, cancel_futures=True)
+        # hand the slot buffers (GBs at config 3) back to the caching allocator
+        # now, not whenever the engine's reference cycles are collected: the
+        # next engine reuses them instead of calling cudaMalloc
+        self.futs.clear()
+        self.cur = None
+        self.slots = []
 
     # -- consumer side (main thread) ------------------------------------------
     def get(self, t):

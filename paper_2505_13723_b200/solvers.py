@@ -320,7 +320,7 @@ class SolverState:
         self._sync()
         if self._e is not None:
             self._it = self._e.t
-            self._e.close()
+            self._e.release()
             self._e = None
 
     @property
@@ -550,6 +550,15 @@ class AdasapEngine:
 
     def close(self):
         self.la.close()
+
+    def release(self):
+        """close() and drop the device buffers (state, operands, workspaces)
+        so the caching allocator can hand them to the next engine at once."""
+        self.close()
+        for name in ("P", "Q", "Y", "G", "g", "WB", "etas", "zop", "zop_next", "ws", "p4ws",
+                     "Pb", "Qb", "W0", "tcp"):
+            if hasattr(self, name):
+                setattr(self, name, None)
 
     # -- one iteration ------------------------------------------------------------
     def step(self, point=None):
@@ -938,7 +947,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
             W_loc = eng.materialize("W")
         W = W_loc if device_out else _to_host64(eng.gather_full(W_loc))
     finally:
-        eng.close()
+        eng.release()
     return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)
 
 
