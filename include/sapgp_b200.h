@@ -261,9 +261,10 @@ int sap_sdd_update(float *V, float *W, float *E, int64_t ldv, int64_t rows, int 
  * u64 = PCG64 (state_hi, state_lo, inc_hi, inc_lo) as numpy's
  * bit_generator.state reports them for a fresh generator. Writes the first
  * `count` normals of stream s to out[s*ldo + i] (fp64), the same values
- * numpy draws (csrc/rng.cu). count <= 2^20. After the stream is done,
- * *sap_normal_status(ws) (a device int) is 0 (ok) or nonzero (raw words ran out /
- * too many rejection draws: fall back to the host draw).
+ * numpy draws (csrc/rng.cu). count <= 2^20. *sap_normal_status(ws) (a device
+ * int the caller zeroes with the workspace) is sticky: 0 while every fill on
+ * this workspace succeeded, nonzero once one ran out of raw words or had too
+ * many rejection draws.
  */
 size_t sap_normal_workspace(int64_t count, int nstreams);
 int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double *out, int64_t ldo,

@@ -382,6 +382,10 @@ int sap_tc_supported(int d, int m) {
 
 // splits for the CTA-pair kernel: whole waves of 74 pairs over 256-row tiles
 int tc2_splits(int64_t b, int64_t tiles) {
+  if (const char *e = getenv("SAP_TC_SPLITS")) {  // experiments: a fixed split count
+    const int s = atoi(e);
+    if (s > 0) return int(std::min<int64_t>(s, std::max<int64_t>(1, tiles)));
+  }
   const int64_t rt = (b + 2 * BM - 1) / (2 * BM);
   const int64_t pairs = kSms / 2;
   int64_t best = 1;

@@ -652,10 +652,8 @@ static int normal_fill_large(const uint64_t *states, int64_t count, double *out,
   using namespace rng;
   LargeWs w;
   large_bytes(count, &w, static_cast<uint8_t *>(ws));
-  int *status = static_cast<int *>(ws);
+  int *status = static_cast<int *>(ws);  // sticky, see sap_normal_fill
   int rc;
-  if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
-    return fail(SAP_ERR_DEVICE, "normal_fill: memset failed");
   const int64_t L = w.L;
   {
     const int64_t threads = (L + kChunk - 1) / kChunk;
@@ -707,8 +705,9 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
   int *code = reinterpret_cast<int *>(w + 256 + size_t(nstreams) * L * 16);
   int *splist = reinterpret_cast<int *>(w + 256 + size_t(nstreams) * L * 20);
   int rc;
-  if (cudaMemsetAsync(status, 0, sizeof(int), st) != cudaSuccess)
-    return fail(SAP_ERR_DEVICE, "normal_fill: memset failed");
+  // the status word is sticky (zeroed by the caller with the workspace; every
+  // fill only raises it), so a failed fill is still reported after the
+  // workspace has been reused
   {
     const int64_t threads = (L + rng::kChunk - 1) / rng::kChunk;
     dim3 grid(unsigned((threads + 255) / 256), unsigned(nstreams));
@@ -727,9 +726,10 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
   return check_launch("normal_emit_kernel");
 }
 
-// status word of the last sap_normal_fill on this workspace (device pointer,
-// the workspace's first int): 0 ok, 1 the generated raw words ran out, 2 too
-// many non-trivial draws for the resolve pass
+// status word of the sap_normal_fill calls on this workspace since the caller
+// zeroed it (device pointer, the workspace's first int; sticky: the worst
+// outcome of any fill): 0 ok, 1 the generated raw words ran out, 2 too many
+// non-trivial draws for the resolve pass
 int *sap_normal_status(void *ws) { return static_cast<int *>(ws); }
 
 }  // extern "C"

@@ -95,7 +95,8 @@ class DeviceNormals:
                                              self.ws.numel() * 8, nat.stream_handle()))
 
     def status(self):
-        """Device int32 status of the last fill (0 = ok); reading it syncs."""
+        """Device int32 status of the fills on this workspace (0 = ok; sticky:
+        a failed fill stays reported after reuse); reading it syncs."""
         return self.ws.view(dtype=__import__("torch").int32)[0]
 
 
@@ -114,5 +115,9 @@ def standard_normal(gen, shape, device=None):
         return gen.standard_normal(shape)
     states = torch.tensor([pcg64_words(gen)], dtype=torch.int64, device=dev)
     out = torch.empty((1, count), dtype=torch.float64, device=dev)
-    DeviceNormals(count, 1, dev).fill(states, out)
+    dn = DeviceNormals(count, 1, dev)
+    dn.fill(states, out)
+    if int(dn.status()) != 0:  # one large draw: checking it costs one sync
+        from .errors import NumericalError
+        raise NumericalError("device normal draw failed (raw stream words ran out)")
     return out.view(shape)

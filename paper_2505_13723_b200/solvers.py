@@ -371,7 +371,8 @@ def _as2d(A):
 
 
 _STAGE = {"buf": None}
-_STAGE_CHUNK = 1 << 24  # elements per staged chunk (64 MB of fp32)
+_STAGE_CHUNK = int(os.environ.get("SAP_READBACK_CHUNK", str(1 << 23)))  # elements per chunk
+_WIDEN_TASKS = int(os.environ.get("SAP_READBACK_TASKS", "8"))
 _READBACK_POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="sap-readback")
 
 
@@ -420,8 +421,8 @@ def _to_host64(t):
         stage[half * chunk: half * chunk + (hi - lo)].copy_(flat[lo:hi], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
-        step = (hi - lo + 3) // 4
-        # four widening tasks per chunk, on disjoint slices of the output
+        step = (hi - lo + _WIDEN_TASKS - 1) // _WIDEN_TASKS
+        # widening tasks per chunk, on disjoint slices of the output
         pend[half] = [_READBACK_POOL.submit(widen, lo, s0, min(hi, s0 + step), half, ev)
                       for s0 in range(lo, hi, step)]
     for fs in pend:
@@ -480,25 +481,31 @@ class AdasapEngine:
         nl = self.shard.size
         self.ld = max(4, (nl + 3) // 4 * 4)
         f32 = torch.float32
+        b, m = self.b, self.m
+        self.use_tc = oracle.use_tc(m) and b >= 16 and nl > 0 and not self.dense
+        self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi) if self.use_tc else None
+        # the lookahead first: its first plans (which need neither Y nor the
+        # state) are produced while the rest of the engine is set up -- the
+        # right-hand sides' upload alone takes ~20 ms at config 3
+        self.t = self.start
+        self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
+                            config.lookahead, identity_precond, tcp=self.tcp, start=self.start)
         self.P = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
         self.Q = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
         self.Y = to_colmajor(Yl, nl, self.dev, self.ld) if nl > 0 else \
             torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
-        b, m = self.b, self.m
         self.G = torch.empty((b, m), dtype=f32, device=self.dev)
         self.g = torch.empty((b, m), dtype=torch.float64, device=self.dev)
         self.WB = torch.zeros((b, m), dtype=f32, device=self.dev)
         self.last_loc = None
         self.etas = torch.zeros(max(self.total or 64, 1), dtype=torch.float64, device=self.dev)
-        self.use_tc = oracle.use_tc(m) and b >= 16 and nl > 0 and not self.dense
         if self.use_tc:
-            self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi)
             self.zop = ZOperand(m, nl, self.dev)
             self.Pb = torch.zeros(self.zop.nz, dtype=f32, device=self.dev)
             self.Qb = torch.zeros(self.zop.nz, dtype=f32, device=self.dev)
             need = nat.load().sap_krows_tc_workspace(b, m, nl)
         else:
-            self.tcp = self.zop = self.Pb = self.Qb = None
+            self.zop = self.Pb = self.Qb = None
             need = nat.load().sap_krows_workspace(b, m, max(nl, 1))
         self.ws = torch.empty(max(need // 4 + 1, 1), dtype=f32, device=self.dev)
         # Phase IV in one launch (sap_block_step, csrc/phase4.cu): gradient
@@ -519,12 +526,9 @@ class AdasapEngine:
             if free > 2 * self.zop.hi.numel() * 2 + (4 << 30):
                 self.zop_next = ZOperand(m, nl, self.dev)
         self.z_stale = True  # zop does not hold Z_t yet (filled by the first step)
-        self.t = self.start
         self.W0 = None  # W at `start` when resuming from a nonzero state (until the first step)
         if state is not None:
             self._load_state(*state)
-        self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
-                            config.lookahead, identity_precond, tcp=self.tcp, start=self.start)
         self.crcs = []
 
     def _load_state(self, W, V, Z):
