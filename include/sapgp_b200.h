@@ -270,6 +270,10 @@ size_t sap_normal_workspace(int64_t count, int nstreams);
 int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double *out, int64_t ldo,
                     void *ws, size_t ws_bytes, void *stream);
 int *sap_normal_status(void *ws);
+/* Device int64: the raw 64-bit words the last fill of MORE than 2^20 normals
+ * consumed from its stream (one stream): PCG64.advance(words) continues the
+ * stream exactly, so a long draw can be produced in chunks. */
+long long *sap_normal_words(void *ws);
 
 /*
  * Host-side draws of iterations t0 .. t0+count-1 (no GPU involved; replaces

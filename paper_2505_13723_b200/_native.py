@@ -65,6 +65,7 @@ SIGNATURES = {
     "sap_normal_workspace": (_SZ, [_I64, _I]),
     "sap_normal_fill": (_I, [_P, _I, _I64, _P, _I64, _P, _SZ, _P]),
     "sap_normal_status": (_P, [_P]),
+    "sap_normal_words": (_P, [_P]),
     "sap_host_draws": (_I, [ctypes.c_uint64, _I64, _I, _I64, _I64, _P, _P, _P, _P, _I]),
     "sap_krows_tc": (_I, [_P, _I64, _I, _P, _I64, _P, _I64, _I64, _P, _P, _I, _I64, _P, _I, _I, _D,
                           _P, _I64, _I, _P, _SZ, _P]),

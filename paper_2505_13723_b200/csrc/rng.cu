@@ -597,9 +597,10 @@ __global__ void __launch_bounds__(kScanBlock) dapply_kernel(
 }
 
 __global__ void emit_large_kernel(const uint64_t *R, int64_t L, int64_t count, const int *off,
-                                  int64_t nch, const int *sp_pos, const int *sp_flags,
-                                  const int *sp_dex, const int *sp_din, const int *sp_cover,
-                                  const double *sp_val, int64_t cap, double *out) {
+                                  int64_t nch, const int *sp_pos, const int *sp_code,
+                                  const int *sp_flags, const int *sp_dex, const int *sp_din,
+                                  const int *sp_cover, const double *sp_val, int64_t cap,
+                                  double *out, long long *words_used) {
   __shared__ double wi[256];
   for (int e = threadIdx.x; e < 256; e += blockDim.x) wi[e] = zig::wi[e];
   __syncthreads();
@@ -620,6 +621,8 @@ __global__ void emit_large_kernel(const uint64_t *R, int64_t L, int64_t count, c
     if (sp_flags[k] != 3) return;
     idx = p - sp_dex[k];
     v = sp_val[k];
+    // the stream position after the last requested draw (continuation)
+    if (idx == count - 1) *words_used = reach_of(sp_pos[k], sp_code[k], L);
   } else {
     if (k >= 0 && sp_cover[k] > p) return;
     idx = p - (k >= 0 ? sp_din[k] : 0);
@@ -628,6 +631,7 @@ __global__ void emit_large_kernel(const uint64_t *R, int64_t L, int64_t count, c
     r >>= 8;
     v = __dmul_rn(double((r >> 1) & 0x000fffffffffffffull), wi[layer]);
     if (r & 1) v = -v;
+    if (idx == count - 1) *words_used = p + 1;  // a one-word draw
   }
   if (idx < count) out[idx] = v;
 }
@@ -680,8 +684,9 @@ static int normal_fill_large(const uint64_t *states, int64_t count, double *out,
                                               w.blk_a, w.blk_b, w.sp_dex, w.sp_din, w.sp_cover,
                                               status);
   emit_large_kernel<<<unsigned((L + 255) / 256), 256, 0, st>>>(
-      w.R, L, count, w.off, w.nch, w.sp_pos, w.sp_flags, w.sp_dex, w.sp_din, w.sp_cover,
-      w.sp_val, w.cap, out);
+      w.R, L, count, w.off, w.nch, w.sp_pos, w.sp_code, w.sp_flags, w.sp_dex, w.sp_din,
+      w.sp_cover, w.sp_val, w.cap, out,
+      reinterpret_cast<long long *>(static_cast<uint8_t *>(ws) + 8));
   return check_launch("normal_emit_large_kernel");
 }
 
@@ -731,5 +736,12 @@ int sap_normal_fill(const uint64_t *states, int nstreams, int64_t count, double 
 // outcome of any fill): 0 ok, 1 the generated raw words ran out, 2 too many
 // non-trivial draws for the resolve pass
 int *sap_normal_status(void *ws) { return static_cast<int *>(ws); }
+
+// raw 64-bit words the last fill of more than 2^20 normals consumed (device
+// int64 at byte 8 of the workspace): advancing the stream's PCG64 by it
+// continues the stream exactly where numpy would draw the next normal
+long long *sap_normal_words(void *ws) {
+  return reinterpret_cast<long long *>(static_cast<uint8_t *>(ws) + 8);
+}
 
 }  // extern "C"

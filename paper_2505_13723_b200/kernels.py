@@ -345,7 +345,13 @@ def ktile(spec, A, asq, aid, C, csq, cid, ldx, d):
 
 
 def to_colmajor(M, n, device, ld=None):
-    """(n x m) host/device matrix -> (m x ld) fp32 device tensor (column-major)."""
+    """(n x m) host/device matrix -> (m x ld) fp32 device tensor (column-major).
+    A CUDA fp32 (n x m) view of a column-major (m x n) buffer with ld == n is
+    adopted without a copy (large right-hand sides built in place)."""
+    if torch.is_tensor(M) and M.is_cuda and M.dtype == torch.float32 and M.ndim == 2 and \
+            M.shape[0] == n and M.stride(0) == 1 and M.stride(1) == n and \
+            (ld is None or ld == n) and torch.device(device) == M.device:
+        return M.T
     if torch.is_tensor(M):
         Mt = M.to(device=device, dtype=torch.float32)
     else:

@@ -121,3 +121,39 @@ def standard_normal(gen, shape, device=None):
         from .errors import NumericalError
         raise NumericalError("device normal draw failed (raw stream words ran out)")
     return out.view(shape)
+
+
+def standard_normal_chunks(gen, rows, cols, device, rows_per_chunk):
+    """``gen.standard_normal((rows, cols))`` drawn on the GPU in row chunks:
+    yields (lo, hi, (hi - lo, cols) float64 device tensor). Each chunk is one
+    device fill of more than 2^20 normals; the fill reports the raw words it
+    consumed (``sap_normal_words``), and the stream's PCG64 state is advanced
+    by exactly that many words on the host (``PCG64.advance``), so chunk k+1
+    starts where numpy would draw the next value. No size limit (the one-shot
+    device draw stops at 2^30 values). ``gen`` must be fresh; it is not
+    modified."""
+    import torch
+    from . import _native as nat
+    from .errors import NumericalError
+    dev = torch.device(device)
+    bg = np.random.PCG64()
+    bg.state = gen.bit_generator.state
+    min_count = (1 << 20) + 1  # the path that reports its consumption
+    # every chunk but the last must be a full fill of its own values (the
+    # reported consumption is that of the fill); only the last may be padded
+    step = max(int(rows_per_chunk), -(-min_count // cols))
+    cap = max(step * cols, min_count)
+    dn = DeviceNormals(cap, 1, dev)
+    buf = torch.empty((1, cap), dtype=torch.float64, device=dev)
+    for lo in range(0, rows, step):
+        hi = min(rows, lo + step)
+        count = max((hi - lo) * cols, min_count)
+        states = torch.tensor([pcg64_words(np.random.Generator(bg))], dtype=torch.int64,
+                              device=dev)
+        dn.count = count
+        dn.fill(states, buf[:, :count])
+        used = int(dn.ws.view(torch.int64)[1].item())  # sap_normal_words
+        if int(dn.status()) != 0:
+            raise NumericalError("device normal draw failed (raw stream words ran out)")
+        bg.advance(used)
+        yield lo, hi, buf[0, :(hi - lo) * cols].view(hi - lo, cols)

@@ -750,8 +750,11 @@ class AdasapEngine:
                  nat.ptr(self.Qb), nat.stream_handle())
 
     # -- materialisation ------------------------------------------------------------
-    def materialize(self, which="W"):
-        """Local shard of W, V or Z as an (n_local x m) fp32 tensor."""
+    def materialize(self, which="W", col=None):
+        """Local shard of W, V or Z as an (n_local x m) fp32 tensor; ``col``:
+        only that right-hand side's column, (n_local x 1) (no n x m buffer)."""
+        if col is not None:
+            return self._materialize_col(which, int(col))
         nl = self.shard.size
         out = torch.empty((self.m, self.ld), dtype=torch.float32, device=self.dev)
         if which == "W":
@@ -776,6 +779,26 @@ class AdasapEngine:
             own = loc >= 0
             W = W.clone()
             W[loc[own]] = self.WB[own]
+        return W
+
+    def _materialize_col(self, which, c):
+        nl = self.shard.size
+        if which == "W" and self.t == self.start:
+            return self.W0[:, c:c + 1].clone() if self.W0 is not None else \
+                torch.zeros((nl, 1), dtype=torch.float32, device=self.dev)
+        if which == "W" and self.dense:
+            return self.Wdense[:, c:c + 1].clone()
+        M = self.M_prev if which == "W" else self.M
+        a, cc = (M[1, 0], M[1, 1]) if which in ("W", "Z") else (M[0, 0], M[0, 1])
+        out = torch.empty((1, self.ld), dtype=torch.float32, device=self.dev)
+        if nl > 0:
+            nat.call("sap_combine", nat.ptr(out), self.ld, nat.ptr(self.P[c]), nat.ptr(self.Q[c]),
+                     self.ld, nl, 1, a, cc, nat.stream_handle())
+        W = out[:, :nl].T.clone()
+        if which == "W":
+            loc = self.last_loc
+            own = loc >= 0
+            W[loc[own], 0] = self.WB[own, c]
         return W
 
     def gather_full(self, local):

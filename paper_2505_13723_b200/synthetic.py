@@ -142,3 +142,75 @@ def make_problem(n, d, family="rbf", m=9, seed=0, lam=1e-2, q=2048,
     return Problem(np.ascontiguousarray(Xall[:n]), y, np.ascontiguousarray(Y),
                    np.ascontiguousarray(Xall[n:]), yall[n:], f_test,
                    family, ls, var, lam)
+
+
+@dataclass
+class DeviceProblem:
+    """``make_problem``'s problem with the right-hand sides built on the device:
+    ``Ycm`` is the (m x n) fp32 column-major buffer the solver adopts without a
+    copy (pass ``Ycm.T``); X, y and the test set stay on the host."""
+    X: np.ndarray
+    y: np.ndarray
+    Ycm: "torch.Tensor"
+    Xtest: np.ndarray
+    ytest: np.ndarray
+    f_test: np.ndarray
+    family: str
+    lengthscales: np.ndarray
+    variance: float
+    lam: float
+
+    @property
+    def n(self):
+        return self.X.shape[0]
+
+    def spec(self):
+        from .kernels import KernelSpec
+        return KernelSpec(self.family, self.lengthscales, self.variance)
+
+
+def make_problem_device(n, d, family="rbf", m=65, seed=0, lam=1e-2, q=2048, device="cuda",
+                        chunk_rows=4_000_000, test_fraction=0.01, test_cap=10_000):
+    """``make_problem`` (pathwise right-hand sides) for sizes whose n x m
+    host arrays would not fit: the same named streams, the prior draws f_s(X)
+    by the fused tensor-core cosine product, zeta by the device sampler in
+    row chunks that continue the numpy stream exactly
+    (``rng.standard_normal_chunks``), each chunk of [y, y - f_s - zeta]
+    written straight into the solver's column-major fp32 layout. Equal to
+    make_problem's arrays up to the fp32 cosine product (~5e-5)."""
+    from .kernels import cos_features_times
+    from .rng import standard_normal_chunks
+    dev = torch.device(device)
+    t = _n_test(n, test_fraction, test_cap)
+    Xall = _all_inputs(n, d, seed, t)
+    ls = np.full(d, math.sqrt(d))
+    var = 1.0
+    freq, ph = feature_map(family, ls, q, substream(seed, "features"))
+    s = m - 1
+    th = np.concatenate([substream(seed, "truth").standard_normal((q, 1)),
+                         substream(seed, "prior").standard_normal((q, s))], axis=1)
+
+    def feats(X, theta):
+        out = cos_features_times(freq, ph, var, X, theta, dev)
+        if out is None:
+            out = torch.as_tensor(features_times(freq, ph, var, X, theta, dev), device=dev)
+        return out
+
+    f_truth = np.empty(n + t)
+    for lo in range(0, n + t, chunk_rows):
+        hi = min(n + t, lo + chunk_rows)
+        f_truth[lo:hi] = feats(Xall[lo:hi], th[:, :1])[:, 0].double().cpu().numpy()
+    yall = f_truth + math.sqrt(lam) * substream(seed, "noise").standard_normal(n + t)
+    ymu, ysd = yall[:n].mean(), yall[:n].std(ddof=1)
+    yall = (yall - ymu) / ysd
+    y = yall[:n]
+    Ycm = torch.empty((m, n), dtype=torch.float32, device=dev)
+    sq = math.sqrt(lam)
+    for lo, hi, z in standard_normal_chunks(substream(seed, "zeta"), n, s, dev, chunk_rows):
+        yc = torch.as_tensor(y[lo:hi], device=dev)
+        f = feats(Xall[lo:hi], th[:, 1:]).double()
+        Ycm[0, lo:hi] = yc.float()
+        Ycm[1:, lo:hi] = (yc[:, None] - f - sq * z).T.float()
+    f_test = feats(Xall[n:], th[:, 1:]).double().cpu().numpy()
+    return DeviceProblem(np.ascontiguousarray(Xall[:n]), y, Ycm, np.ascontiguousarray(Xall[n:]),
+                         yall[n:], f_test, family, ls, var, lam)

@@ -128,3 +128,24 @@ def test_device_normals_large_counts(count):
     got = out[0].cpu().numpy()
     mism = assert_numpy_equal(got, g.standard_normal(count), count)
     assert mism <= max(8, count // 200_000)
+
+
+@pytest.mark.gpu
+def test_chunked_stream_continues_exactly():
+    """A long draw in device chunks, each continuing the PCG64 stream by the
+    raw words the previous fill reports (sap_normal_words), equals numpy's one
+    draw (up to the 1-ulp log1p tail values)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2505_13723_b200.rng import standard_normal_chunks, substream
+    rows, cols = 70_001, 64                     # 4.48M values, chunks of 20000 rows
+    ref = substream(3, "zeta").standard_normal((rows, cols))
+    got = np.empty_like(ref)
+    for lo, hi, chunk in standard_normal_chunks(substream(3, "zeta"), rows, cols, "cuda", 20_000):
+        got[lo:hi] = chunk.cpu().numpy()
+    bad = np.flatnonzero(got.ravel() != ref.ravel())
+    assert bad.size <= 8, bad[:10]
+    if bad.size:
+        g, r = got.ravel()[bad], ref.ravel()[bad]
+        assert np.all(np.nextafter(r, g) == g) and np.all(np.abs(r) > 3.6)
