@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "sapgp_b200.h")
 
 def declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long|const char \*|int \*)\s*(sap_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long \*|long long|const char \*|int \*)\s*(sap_\w+)\(", text, re.M)))
 
 
 def test_header_declares_the_boundary():
