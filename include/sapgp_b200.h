@@ -349,6 +349,10 @@ typedef struct sap_step_args {
 
 enum { SAP_STEP_GRAD = 1, SAP_STEP_APPLY = 2 };
 
+/* 1 if sap_block_step handles these shapes (m <= 128 and the staged tiles fit
+ * shared memory), else 0 (callers use the unfused kernels). */
+int sap_block_step_supported(int64_t b, int r, int m);
+
 /* Workspace bytes of sap_block_step / sap_woodbury_apply; the first 256
  * bytes (grid barrier) must be zeroed once before the first call. */
 size_t sap_block_step_workspace(int64_t b, int r, int m);

@@ -73,6 +73,7 @@ SIGNATURES = {
                                _I, _D, _P, _I64, _I, _P, _SZ, _I, _P, _P, _P, _I64, _D, _D, _P,
                                _P, _P, _P, _P, _P]),
     "sap_block_step_workspace": (_SZ, [_I64, _I, _I]),
+    "sap_block_step_supported": (_I, [_I64, _I, _I]),
     "sap_block_step": (_I, [_P, _I, _P, _SZ, _P]),
     "sap_woodbury_apply": (_I, [_P, _P, _I64, _I64, _I, _P, _I64, _I, _P, _P, _I64, _P, _SZ, _P]),
     "sap_sym_eig_workspace": (_SZ, [_I, _I]),

@@ -436,6 +436,10 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 extern "C" {
 
+int sap_block_step_supported(int64_t b, int r, int m) {
+  return (b > 0 && r >= 0 && m > 0 && m <= 128 && p4::smem_bytes(m, r) <= kSmemMax) ? 1 : 0;
+}
+
 size_t sap_block_step_workspace(int64_t b, int r, int m) {
   if (b <= 0 || r < 0 || m <= 0) return 0;
   const size_t rm = size_t(r) * size_t(m);

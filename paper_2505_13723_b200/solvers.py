@@ -512,8 +512,9 @@ class AdasapEngine:
         # gather + Woodbury apply + lazy update + the next operand's block rows;
         # SAP_FUSED_STEP=0 selects the unfused chain (grad_gather, two GEMMs,
         # pq_update, separate operand pass) for A/B runs
-        self.fused = os.environ.get("SAP_FUSED_STEP", "1") == "1" and not self.dense
         lib = nat.load()
+        self.fused = (os.environ.get("SAP_FUSED_STEP", "1") == "1" and not self.dense
+                      and bool(lib.sap_block_step_supported(b, self.r, m)))
         self.p4ws = torch.zeros(lib.sap_block_step_workspace(b, self.r, m) // 8 + 1,
                                 dtype=torch.float64, device=self.dev)
         self.zflag = torch.zeros(2, dtype=torch.int32, device=self.dev)

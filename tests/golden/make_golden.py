@@ -218,19 +218,27 @@ def config3():
         out[f"{fam}_B"] = B
         out[f"{fam}_G"] = rdist.col_dist_matmul(orc, Z, B, pool)
     del Z
-    # 5 iterations of the reference solver
+    # 5 iterations of the reference solver, through its own step function
+    # (adasap_solve would end with the relative residual, an n x n x m
+    # product: hours at n = 1e6 in numpy)
     spec = sapgp.KernelSpec("matern32", np.full(d, np.sqrt(d)), 1.0)
     orc = sapgp.KernelOracle(spec, X, 1e-2)
     Y = substream(seed, "golden_y3").standard_normal((n, m))
     cfg = sapgp.RunConfig(lam=1e-2, blocksize=b, nystrom_rank=100, residual_every=0, seed=seed,
                           max_iters=5)
-    res = rsol.adasap_solve(orc, Y, cfg, pool=pool)
+    accel = rsol.resolve_accel(cfg, n, b)
+    state = rsol.SolverState.zeros(n, m, accelerated=True)
+    crcs, etas = [], []
+    for _ in range(5):
+        state, eta, block = rsol.adasap_step(orc, state, Y, cfg, accel, pool)
+        crcs.append(rsol._block_hash(block))
+        etas.append(eta)
     rows = sample_rows(n)
     out["traj_rows"] = rows
-    out["traj_W_rows"] = res.W[rows]
-    out["traj_W_colnorm"] = np.linalg.norm(res.W, axis=0)
-    out["traj_crc"] = np.array([rec.block_hash for rec in res.trace.records], dtype=np.int64)
-    out["traj_eta"] = np.array([rec.stepsize for rec in res.trace.records])
+    out["traj_W_rows"] = state.W[rows]
+    out["traj_W_colnorm"] = np.linalg.norm(state.W, axis=0)
+    out["traj_crc"] = np.array(crcs, dtype=np.int64)
+    out["traj_eta"] = np.array(etas)
     pool.close()
     np.savez_compressed(os.path.join(HERE, "config3.npz"), **out)
 

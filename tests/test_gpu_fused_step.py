@@ -242,3 +242,23 @@ def test_fused_solver_follows_unfused(fam, monkeypatch):
     # iteration (measured 1.1e-5 for RBF after 120 iterations) -- well inside
     # the block-product bar of 1e-4
     assert np.abs(a.W - b.W).max() / np.abs(b.W).max() < 1e-4
+
+
+def test_shapes_outside_the_fused_step_fall_back():
+    """m > 128 right-hand sides: the fused Phase IV (and the tensor-core
+    product) do not apply; the solver takes the unfused kernels and still
+    follows the oracle."""
+    from oracle import sapgp_oracle as orc
+    rng = np.random.default_rng(9)
+    n, d, m = 2500, 5, 130
+    X = rng.standard_normal((n, d))
+    Y = rng.standard_normal((n, m))
+    assert not nat.load().sap_block_step_supported(256, 32, m)
+    o = sap.KernelOracle(sap.KernelSpec("rbf", np.full(d, 1.5), 1.0), X, 1e-1, device=0)
+    cfg = sap.RunConfig(lam=1e-1, blocksize=256, nystrom_rank=32, max_iters=10, residual_every=0,
+                        seed=2)
+    res = sap.adasap_solve(o, Y, cfg)
+    Wref, etas, crcs, _ = orc.adasap_solve(orc.Points("rbf", np.full(d, 1.5), 1.0, X), 1e-1, Y,
+                                           10, 2, 256, 32)
+    assert [r.block_hash for r in res.trace.records] == list(crcs)
+    assert np.abs(res.W - Wref).max() / np.abs(Wref).max() < 1e-3

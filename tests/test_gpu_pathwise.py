@@ -38,3 +38,18 @@ def test_device_resident_pathwise_matches_host_path():
     # fp32 cosine features on the tensor cores vs the fp64 host product: ~5e-5
     assert np.abs(dev.sample_values - ref).max() / np.abs(ref).max() < 1e-3
     assert np.abs(dev.mean_values - host.mean_values).max() / np.abs(host.mean_values).max() < 1e-4
+
+
+def test_device_problem_builder_matches_host_generator():
+    """synthetic.make_problem_device (the n = 1e8 path: chunked device zeta
+    continuing the numpy stream, fused cosine products, column-major fp32)
+    equals make_problem's host arrays up to the fp32 cosine product."""
+    n, d, m = 30_000, 9, 17
+    host = synthetic.make_problem(n, d, "matern32", m, seed=4, lam=1e-2)
+    dev = synthetic.make_problem_device(n, d, "matern32", m, seed=4, lam=1e-2, device="cuda",
+                                        chunk_rows=7_000)
+    assert np.array_equal(dev.X, host.X) and np.array_equal(dev.Xtest, host.Xtest)
+    np.testing.assert_allclose(dev.y, host.y, rtol=0, atol=1e-4)
+    Y = dev.Ycm.T.double().cpu().numpy()
+    assert np.abs(Y - host.Y).max() / np.abs(host.Y).max() < 1e-4
+    assert np.abs(dev.f_test - host.f_test).max() / np.abs(host.f_test).max() < 1e-4
