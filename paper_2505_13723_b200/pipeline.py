@@ -515,7 +515,8 @@ class Lookahead:
             eta_ready.record(self.main)
         if self.timings is not None:
             self.timings.append(dict(count=count, rng=tm1 - tm0, gpu_wait=tm2 - tm1,
-                                     factor=tm3 - tm2, total=time.perf_counter() - tm0))
+                                     factor=tm3 - tm2, total=time.perf_counter() - tm0,
+                                     start=tm0, end=time.perf_counter()))
         return _Batch(slot, t0, count, blocks, crcs, rho, Ss, ready, eta_ready, owner)
 
     def _produce_blocks(self, slot, t0, count, side, owner):

@@ -25,6 +25,11 @@ for rep in range(8):
         if dt > 5e-3:
             slow.append((k + 1, round(dt * 1e3, 1)))
     torch.cuda.synchronize(); T.append(time.perf_counter())
+    if st._e is not None and st._e.la.timings is not None:  # SAP_PROFILE=1
+        for tm in sorted(st._e.la.timings, key=lambda x: x["start"]):
+            print(f"   batch count={tm['count']:3d} start {1e3 * (tm['start'] - T[1]):7.1f} "
+                  f"end {1e3 * (tm['end'] - T[1]):7.1f} ms (rng {1e3 * tm['rng']:.1f}, "
+                  f"enqueue {1e3 * tm['gpu_wait']:.1f}, factor {1e3 * tm['factor']:.1f})")
     W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
     st.iteration = st.iteration; T.append(time.perf_counter())
     names = ["oracle", "bind+step0", "19 steps", "W readback", "close"]
