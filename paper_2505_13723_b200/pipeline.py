@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import os
 import sys
+import threading
 import time
 import warnings
 from concurrent.futures import ThreadPoolExecutor
@@ -130,6 +131,8 @@ class _Batch:
 class Lookahead:
     """Produces IterPlan(t) for t = start..total-1 (total None: unbounded) in
     batches of up to ``L``."""
+
+    _WIDTH = int(os.environ.get("SAP_PRODUCE_WIDTH", "2"))  # batches produced concurrently
 
     def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
                  tcp=None, start=0):
@@ -240,6 +243,7 @@ class Lookahead:
         self.cur = None
         self.k = -1  # batch currently consumed
         self.futs = {}
+        self._gate = {}  # batch -> Event: its production has been enqueued
         for k in range(self.depth):
             if self._has_batch(k):
                 self._submit(k)
@@ -256,8 +260,24 @@ class Lookahead:
         t0, t1 = self.bounds[k], self.bounds[k + 1]
         ns = len(self.slots)
         owner = k % self.shard.world
-        self.futs[k] = self.pool.submit(self._produce, self.slots[k % ns], t0, t1 - t0,
+        self._gate[k] = threading.Event()
+        self.futs[k] = self.pool.submit(self._gated, k, self.slots[k % ns], t0, t1 - t0,
                                         self.sides[k % ns], owner)
+
+    def _gated(self, k, *args):
+        """Batch k's host-side production starts once batch k - _WIDTH has
+        been enqueued: a fresh engine submits its first ``depth`` batches at
+        once, and six producers sharing the GIL took ~35 ms to enqueue the
+        one-iteration batch 0 that the first step waits for (~5 ms alone).
+        In steady state the gate is long open when a batch is submitted."""
+        prev = self._gate.get(k - self._WIDTH)
+        if prev is not None:
+            prev.wait()
+            self._gate.pop(k - self._WIDTH, None)
+        try:
+            return self._produce(*args)
+        finally:
+            self._gate[k].set()
 
     def close(self):
         # batches not started yet are dropped; running producers finish their
@@ -283,7 +303,9 @@ class Lookahead:
                 raise ContractError(f"iteration {t} is past the solver's iteration budget "
                                     f"({self.total})")
             self.k += 1
+            xfer.mark(f"get batch {self.k}")
             cur = self.futs.pop(self.k).result()
+            xfer.mark(f"got batch {self.k}")
             main.wait_event(cur.ready)
             if self.shard.world > 1:
                 self._share(cur)
@@ -393,8 +415,9 @@ class Lookahead:
         if slot.h2d_done is not None:
             slot.h2d_done.synchronize()  # pinned inputs of the previous use consumed
         tm0 = time.perf_counter()
-
+        xfer.mark(f"produce {t0}+{count} start")
         blocks, crcs = self._host_draws(slot, t0, count, omega=bool(r), v0=True)
+        xfer.mark("draws")
         tm1 = time.perf_counter()
         pts = self.o.points
         fs = self.fast if self.fast is not None else side
@@ -409,22 +432,29 @@ class Lookahead:
                 slot.states[:count].copy_(slot.h_states[:count], non_blocking=True)
                 om = slot.omega[:count]
                 slot.normals.fill(slot.states, om.view(count, b * r), nstreams=count)
+            xfer.mark("normals")
             bd = slot.block_dev[:count]
             slot.loc_dev[:count].copy_(self.shard.local_positions(bd))
+            xfer.mark("loc")
             sketch = torch.empty((count, b, max(r, 1)), dtype=torch.float32, device=self.dev)
+            xfer.mark("empty")
             # the batch's gathers, feature conversions and column bounds in one
             # launch each; per iteration only the sketch's Z operand and product
             flat = bd.reshape(-1)
             pts.gather(flat, out=(slot.Xb[:count].view(-1, pts.ldx), slot.rsq[:count].view(-1)))
+            xfer.mark("gather")
             if self.tcp is not None:
                 self.tcp.gather_rows_batch(bd, slot.RAg[:count])
+                xfer.mark("gather rows")
             if r and self.sketch_gemm:
                 # K_BB once per iteration (the power iteration's operand too),
                 # then the sketch K_BB Omega as one batched fp32 GEMM
                 # (row_dist_matmul, dist.py:130-147; 2 b^2 r flop per iteration)
                 K.ktile_f32_batch(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
                                   slot.Kbb[:count])
+                xfer.mark("kbb")
                 torch.bmm(slot.Kbb[:count, :, :b], om.to(torch.float32), out=sketch)
+                xfer.mark("sketch")
             elif r:
                 omc = om.transpose(1, 2).to(torch.float32).contiguous()  # (count, r, b) RHS
                 if self.tc_sketch:
@@ -461,8 +491,10 @@ class Lookahead:
             # eigensolves included (sap_sym_eig_batch): no host round trip;
             # failures and warnings ride on the plan flags (check_flags)
             with torch.cuda.device(self.dev), torch.cuda.stream(fs):
+                xfer.mark("gram")
                 W, S, rho_d, Mc, E, flags = factor_gram_batch(
                     G[:, :r, :r], G[:, r:, :r], G[:, r:, r:], r, self.lam)
+                xfer.mark("factor")
                 tm2 = time.perf_counter()
                 torch.bmm(Y, W, out=slot.U[:count])
                 slot.Mc[:count].copy_(Mc)
@@ -503,6 +535,7 @@ class Lookahead:
                                  slot.E[q0:q1], slot.rho[q0:q1], slot.v0[q0:q1], self.lam,
                                  self.iters, slot.eta[q0:q1], slot.bad[q0:q1])
             torch.div(slot.eta[:count], slot.rho[:count], out=slot.eta_rho[:count])
+            xfer.mark("power")
             ready = torch.cuda.Event()
             ready.record(self.main)
             slot.h2d_done = ready  # pinned host buffers reusable after this point

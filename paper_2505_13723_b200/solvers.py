@@ -38,7 +38,6 @@ import ctypes
 import math
 import os
 import time
-from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -373,7 +372,6 @@ def _as2d(A):
 _STAGE = {"buf": None}
 _STAGE_CHUNK = int(os.environ.get("SAP_READBACK_CHUNK", str(1 << 23)))  # elements per chunk
 _WIDEN_TASKS = int(os.environ.get("SAP_READBACK_TASKS", "8"))
-_READBACK_POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="sap-readback")
 
 
 def _staging(elems):
@@ -423,7 +421,7 @@ def _to_host64(t):
         ev.record(stream)
         step = (hi - lo + _WIDEN_TASKS - 1) // _WIDEN_TASKS
         # widening tasks per chunk, on disjoint slices of the output
-        pend[half] = [_READBACK_POOL.submit(widen, lo, s0, min(hi, s0 + step), half, ev)
+        pend[half] = [xfer.host_pool().submit(widen, lo, s0, min(hi, s0 + step), half, ev)
                       for s0 in range(lo, hi, step)]
     for fs in pend:
         if fs is not None:
@@ -488,12 +486,15 @@ class AdasapEngine:
         # state) are produced while the rest of the engine is set up -- the
         # right-hand sides' upload alone takes ~20 ms at config 3
         self.t = self.start
+        xfer.mark("bind: tc points")
         self.la = Lookahead(oracle, self.shard, config.seed, b, self.r, self.lam, self.total,
                             config.lookahead, identity_precond, tcp=self.tcp, start=self.start)
+        xfer.mark("bind: lookahead")
         self.P = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
         self.Q = torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
         self.Y = to_colmajor(Yl, nl, self.dev, self.ld) if nl > 0 else \
             torch.zeros((self.m, self.ld), dtype=f32, device=self.dev)
+        xfer.mark("bind: Y upload")
         self.G = torch.empty((b, m), dtype=f32, device=self.dev)
         self.g = torch.empty((b, m), dtype=torch.float64, device=self.dev)
         self.WB = torch.zeros((b, m), dtype=f32, device=self.dev)
@@ -526,6 +527,7 @@ class AdasapEngine:
             free, _ = torch.cuda.mem_get_info(self.dev)
             if free > 2 * self.zop.hi.numel() * 2 + (4 << 30):
                 self.zop_next = ZOperand(m, nl, self.dev)
+        xfer.mark("bind: buffers")
         self.z_stale = True  # zop does not hold Z_t yet (filled by the first step)
         self.W0 = None  # W at `start` when resuming from a nonzero state (until the first step)
         if state is not None:

@@ -18,11 +18,37 @@ def snapshot():
         return dict(_bytes)
 
 
+# SAP_TRACE=1: (time, thread, tag) marks of the bind and the lookahead
+# producers (diagnosis: scripts/e2e_phases.py prints them)
+import os as _os
+import time as _time
+
+TRACE = [] if _os.environ.get("SAP_TRACE") == "1" else None
+
+
+def mark(tag):
+    if TRACE is not None:
+        TRACE.append((_time.perf_counter(), threading.current_thread().name, tag))
+
+
 # ---------------------------------------------------------------------------
 # host -> device uploads of large numpy arrays through a pinned double buffer
 
 _UP = {"buf": None}
 _UP_CHUNK = 1 << 23  # elements per chunk
+_TASKS = 8           # host conversion tasks per chunk
+_POOL = {"ex": None}
+_POOL_LOCK = threading.Lock()
+
+
+def host_pool():
+    """Process-wide host threads for the large casting copies of uploads and
+    readbacks (numpy's casting copy releases the GIL)."""
+    with _POOL_LOCK:
+        if _POOL["ex"] is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _POOL["ex"] = ThreadPoolExecutor(max_workers=_TASKS, thread_name_prefix="sap-host")
+        return _POOL["ex"]
 
 
 def _up_staging(nbytes):
@@ -38,12 +64,12 @@ def upload(A, dtype, device):
     """numpy array -> new contiguous device tensor of ``dtype`` (same shape).
 
     Host threads convert/copy chunk k into one half of a pinned buffer while
-    the DMA of chunk k-1 from the other half runs: pageable uploads (~11 GB/s
-    here) would otherwise dominate a solve's setup. Values are rounded exactly
-    as a device-side cast would (round to nearest)."""
+    the DMA of chunk k-1 from the other half runs and the conversion of chunk
+    k-1 finishes: pageable uploads (~11 GB/s here) would otherwise dominate a
+    solve's setup. Values are rounded exactly as a device-side cast would
+    (round to nearest)."""
     import numpy as np
     import torch
-    from concurrent.futures import ThreadPoolExecutor
     A = np.ascontiguousarray(A)
     np_dt = {torch.float32: np.float32, torch.float64: np.float64}[dtype]
     out = torch.empty(A.shape, dtype=dtype, device=device)
@@ -58,22 +84,34 @@ def upload(A, dtype, device):
     stage = _up_staging(chunk * esz)
     halves = [stage[h * chunk * esz:(h + 1) * chunk * esz].view(dtype) for h in range(2)]
     stream = torch.cuda.current_stream(device)
+    ex = host_pool()
     done = [None, None]  # event: the half's last DMA finished reading it
-    with ThreadPoolExecutor(max_workers=4) as ex:
-        for k, lo in enumerate(range(0, total, chunk)):
-            hi = min(total, lo + chunk)
-            h = k & 1
-            if done[h] is not None:
-                done[h].synchronize()
-            dst = halves[h][:hi - lo].numpy()
-            step = (hi - lo + 3) // 4
-            list(ex.map(lambda s0: np.copyto(dst[s0 - lo:min(hi, s0 + step) - lo],
-                                             flat_in[s0:min(hi, s0 + step)], casting="same_kind"),
-                        range(lo, hi, step)))
-            flat_out[lo:hi].copy_(halves[h][:hi - lo], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            done[h] = ev
+
+    def convert(dst, lo, s0, s1):
+        np.copyto(dst[s0 - lo:s1 - lo], flat_in[s0:s1], casting="same_kind")
+
+    def dma(k, lo, hi, futs):
+        for f in futs:
+            f.result()
+        h = k & 1
+        flat_out[lo:hi].copy_(halves[h][:hi - lo], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        done[h] = ev
+
+    prev = None
+    for k, lo in enumerate(range(0, total, chunk)):
+        hi = min(total, lo + chunk)
+        h = k & 1
+        if done[h] is not None:
+            done[h].synchronize()
+        dst = halves[h][:hi - lo].numpy()
+        step = (hi - lo + _TASKS - 1) // _TASKS
+        futs = [ex.submit(convert, dst, lo, s0, min(hi, s0 + step)) for s0 in range(lo, hi, step)]
+        if prev is not None:
+            dma(*prev)
+        prev = (k, lo, hi, futs)
+    dma(*prev)
     for ev in done:
         if ev is not None:
             ev.synchronize()

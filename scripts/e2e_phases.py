@@ -30,6 +30,12 @@ for rep in range(8):
             print(f"   batch count={tm['count']:3d} start {1e3 * (tm['start'] - T[1]):7.1f} "
                   f"end {1e3 * (tm['end'] - T[1]):7.1f} ms (rng {1e3 * tm['rng']:.1f}, "
                   f"enqueue {1e3 * tm['gpu_wait']:.1f}, factor {1e3 * tm['factor']:.1f})")
+    from paper_2505_13723_b200 import xfer
+    if xfer.TRACE is not None:  # SAP_TRACE=1
+        for tt, th, tag in xfer.TRACE:
+            if tt >= T[1]:
+                print(f"   {1e3 * (tt - T[1]):8.2f} ms  {th:22s} {tag}")
+        xfer.TRACE.clear()
     W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
     st.iteration = st.iteration; T.append(time.perf_counter())
     names = ["oracle", "bind+step0", "19 steps", "W readback", "close"]
