@@ -72,7 +72,8 @@ struct Args {
   int rows_per;    // block rows per CTA
   int do_grad, do_apply, has_next;
   int stage;       // 0: A+B, 2: D (+E); C is phase4_reduce_kernel
-  int dbg;         // profiling: 5 skips B's product, 6 D's product, 7 the update
+  int dbg;         // profiling: 5 skips B's product, 6 D's product, 7 the update,
+                   // 8 the rebuild check (E), 9 the next operand's block rows
 };
 
 // Shared-memory carve-up (doubles unless noted); m8 = m rounded up to 8,
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
         if (a.Pb) atomicMax(reinterpret_cast<int *>(sbound + c), __float_as_int(fabsf(pn)));
         if (a.Qb && a.Qw)
           atomicMax(reinterpret_cast<int *>(sbound + m + c), __float_as_int(fabsf(qn)));
-        if (A.has_next) {
+        if (A.has_next && A.dbg != 9) {
           const float sc = szs[c];
           float z = (zp1 * sc) * pn;
           if (a.Qw) z = fmaf(zq1 * sc, qn, z);
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
     if (a.Qb && a.Qw && sbound[m + c] > 0.0f)
       atomicMax(reinterpret_cast<int *>(a.Qb + c), __float_as_int(sbound[m + c]));
   }
-  if (!A.has_next) return;
+  if (!A.has_next || A.dbg == 8) return;
   if (__syncthreads_or(over) && tid == 0) atomicOr(a.zflag + a.flag_idx, 1);
   // ---------------- E: rebuild the next operand if its scale was left ----------------
   // The last CTA to finish reads the flag (threadfence reduction pattern). The

@@ -62,6 +62,10 @@ for dbg in ("5", "6", "7", "0"):
     os.environ["SAP_P4_DEBUG"] = dbg
     print("GRAD|APPLY dbg %s (5: no B product, 6: no D product, 7: no update): %.1f us"
           % (dbg, timeit(3, False)))
+for dbg in ("8", "9"):
+    os.environ["SAP_P4_DEBUG"] = dbg
+    print("GRAD|APPLY + next dbg %s (8: no rebuild check, 9: no operand rows): %.1f us"
+          % (dbg, timeit(3, True)))
 os.environ["SAP_P4_DEBUG"] = "0"
 print("GRAD        %.1f us" % timeit(1, False))
 print("GRAD|APPLY + next %.1f us" % timeit(3, True))
