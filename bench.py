@@ -180,9 +180,9 @@ def b_pad_rows(b):
     return (b + 255) // 256 * 256  # block rows the CTA-pair kernel computes
 
 
-# The lookahead produces plans in batches that ramp 1, 2, 4, ..., 32 over the
-# first 63 iterations (pipeline.Lookahead); those iterations are not steady
-# state, so they count as warm-up whatever --warmup asks for.
+# The lookahead produces plans in batches that ramp 1, 4, 16, then full
+# batches from iteration 21 (pipeline.Lookahead); the first iterations are
+# not steady state, so 64 count as warm-up whatever --warmup asks for.
 RAMP_ITERS = 64
 
 

@@ -14,7 +14,7 @@ block-row product and the update depends only on (seed, t) and X:
 so they are produced in batches by ``depth`` (default 6) host producer
 threads, up to ``depth`` batches ahead of the block-row products that
 consume them; their GPU work is enqueued in order on the solver's stream
-(see Lookahead.__init__). Batch sizes ramp 1, 2, 4, ... up to
+(see Lookahead.__init__). Batch sizes ramp 1, 4, 16, ... up to
 ``L = config.lookahead`` so the first iteration waits for one plan only, not
 for a full batch. The host draws the blocks (numpy-exact, csrc/host_rng.cu)
 and enqueues; everything else runs on the GPU with no device->host round
@@ -133,6 +133,7 @@ class Lookahead:
     batches of up to ``L``."""
 
     _WIDTH = int(os.environ.get("SAP_PRODUCE_WIDTH", "2"))  # batches produced concurrently
+    _RAMP = max(2, int(os.environ.get("SAP_RAMP", "4")))    # batch-size growth of the ramp
 
     def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
                  tcp=None, start=0):
@@ -217,8 +218,12 @@ class Lookahead:
                 _l, _ = torch.linalg.cholesky_ex(_a)
                 torch.cholesky_inverse(_l)
                 torch.linalg.solve_triangular(_l, _a, upper=False)
-        # batch k covers iterations [bounds[k], bounds[k+1]); sizes ramp 1, 2,
-        # 4, ... up to L, extended on demand (_has_batch)
+        # batch k covers iterations [bounds[k], bounds[k+1]); sizes ramp 1, 4,
+        # 16, ... up to L, extended on demand (_has_batch). Growth 4 rather
+        # than 2: a batch's host-side cost is mostly per batch, not per
+        # iteration, and fewer ramp batches kept a fresh engine's first 20
+        # steps from waiting on production (34-36 ms against 38-41 ms with
+        # 1, 2, 4, 8, 16; scripts/e2e_phases.py, SAP_RAMP)
         self.bounds = [int(start)]
         self._c = 1
         # depth producers: a batch's production (host RNG -> sketch on the GPU ->
@@ -253,7 +258,7 @@ class Lookahead:
         while len(self.bounds) <= k + 1 and (self.total is None or self.bounds[-1] < self.total):
             nxt = self.bounds[-1] + self._c
             self.bounds.append(nxt if self.total is None else min(self.total, nxt))
-            self._c = min(2 * self._c, self.L)
+            self._c = min(self._RAMP * self._c, self.L)
         return len(self.bounds) > k + 1
 
     def _submit(self, k):

@@ -7,7 +7,9 @@ from torch.profiler import profile, ProfilerActivity
 import paper_2505_13723_b200 as sap
 from paper_2505_13723_b200 import synthetic
 from paper_2505_13723_b200.solvers import AdasapEngine
-n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
+# config 3 by default; N=100000 D=11 B=1000 FAM=rbf for config 2
+n, d, b = int(os.environ.get("N", "1000000")), int(os.environ.get("D", "9")), int(os.environ.get("B", "2000"))
+m, r = 65, 100
 prob = synthetic.make_problem(n, d, os.environ.get("FAM", "matern32"), m, seed=0, lam=1e-2, device="cuda", rhs="noise")
 o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
 WARM, NIT = int(os.environ.get("WARM", "64")), int(os.environ.get("NIT", "64"))
@@ -46,7 +48,7 @@ for e in ev:
 for sid, es in streams.items():
     print(f"stream {sid}: {len(es)} kernels, {sum(e['dur'] for e in es)/NIT:.1f} us/iter")
 # krows kernels: duration stats
-kr = [e["dur"] for e in ev if "krows_tc2_kernel<1, 80" in e["name"]]
+kr = [e["dur"] for e in ev if "krows_tc2_kernel<" in e["name"] and ", 80," in e["name"]]
 print("krows us:", [round(x) for x in kr[:NIT]])
 # per-kernel totals per iteration, by stream
 agg = {}

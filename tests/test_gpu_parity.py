@@ -299,7 +299,7 @@ def test_tensor_core_edge_shapes(n, d, b, m):
 
 
 def test_long_trajectory_full_lookahead_batches():
-    """80 iterations: the lookahead ramps 1, 2, 4, 8, 16 to full 32-iteration
+    """80 iterations: the lookahead ramps 1, 4, 16 to full 32-iteration
     batches (batched gathers, K_BB tiles and power iterations, stepsizes
     copied to the trace once per batch, 1/rho folded into the update's
     stepsize); blocks, stepsizes and the iterate against the oracle."""
