@@ -313,7 +313,7 @@ def run_b200(args):
                                "fp16 passes, nz=%d) at the measured bf16 peak over the "
                                "measured kernel time" % (g1, ka, nz)}
         # the epilogue's special-function bound: ex2 (RBF) or rsqrt + ex2 (Matern) per
-        # kernel entry on the MUFU pipe (16 lanes/clk/SM, scripts/micro/pipes.cu)
+        # kernel entry on the MUFU pipe (16 lanes/clk/SM for every MUFU op, scripts/micro/mufu.cu)
         mufu_ops = 1 if args.family == "rbf" else 2
         mufu_ms = b_pad_rows(b) * n_local * mufu_ops / (16 * 148 * 1.965e9) * 1e3
         tensor_pipe["mufu_bound_ms"] = mufu_ms
