@@ -59,6 +59,9 @@ __device__ __forceinline__ unsigned long long prof_clock() {
 
 constexpr int NT = 128;     // points per column tile (64 staged per CTA)
 constexpr int NB = 3;       // S/P tiles in flight in TMEM (columns 0..383)
+#ifndef SAP_EPI_STAGGER
+#define SAP_EPI_STAGGER -1  // cycles; -1: the per-family default (kStagger)
+#endif
 #ifndef SAP_KSEG
 #define SAP_KSEG 16
 #endif
@@ -444,6 +447,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
       }
     };
+    // Matern: warpgroups 0-1 start ~0.4 tile later than 2-3, so the two
+    // halves of every sub-partition's epilogue warps run out of phase: one
+    // half's per-tile serial part (TMEM load/store waits, barrier arrive)
+    // overlaps the other half's MUFU work instead of all four idling the
+    // MUFU pipe together (config 3: -1.6%; RBF, whose epilogue is not
+    // MUFU-bound, +0.4%, so 0 there; SAP_EPI_STAGGER overrides)
+    constexpr long long kStagger =
+        SAP_EPI_STAGGER >= 0 ? SAP_EPI_STAGGER
+                             : ((FAM == SAP_MATERN32 || FAM == SAP_MATERN52) ? 1200 : 0);
+    if (kStagger > 0 && w < 2) {
+      const long long t0 = clock64();
+      while (clock64() - t0 < kStagger) {
+      }
+    }
     for (int k = 0;; ++k) {
       const int u = take_unit(k, false);
       if (dyn) {  // one arrival per warp
