@@ -528,10 +528,12 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
     unsigned long long h[148 * 16];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost);
-    const char *names[12] = {"prod.wait_empty", "prod.issue", "mma.wait_full", "mma.wait_pfull",
+    const char *names[16] = {"prod.wait_empty", "prod.issue", "mma.wait_full", "mma.wait_pfull",
                              "mma.wait_gempty", "mma.issue_g1", "mma.issue_g2", "epi.wait_sfull",
-                             "epi.convert", "epi.arrive", "epi.drain", "kernel"};
-    for (int k = 0; k < 12; ++k) {
+                             "epi.convert", "epi.arrive", "epi.drain", "kernel",
+                             "epi.first_tile_at", "epi.done_at", "sidejob.done_at",
+                             "epi.take_unit"};
+    for (int k = 0; k < 16; ++k) {
       double s0 = 0, s1 = 0; int n0 = 0, n1 = 0;
       for (int g = 0; g < grid; ++g) {
         if (g % 2 == 0) { s0 += h[g * 16 + k]; ++n0; } else { s1 += h[g * 16 + k]; ++n1; }

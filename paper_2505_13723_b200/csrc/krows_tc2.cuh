@@ -390,6 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // path between two block-row products. The block rows are patched by
     // the Phase IV kernel after the update (phase4.cu).
     if (p.zn.Zhi) zop::next_pass(p.zn, blockIdx.x, gridDim.x, (warp - 2) * 32 + lane, 64);
+    if (p.prof && warp == 2 && lane == 0) p.prof[blockIdx.x * 16 + 14] = prof_clock() - kstart;
   } else {
     // ===================== epilogue (both CTAs) =====================
     // Four warpgroups, i.e. four warps per SM sub-partition, so TMEM load/store
@@ -413,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int c = 0; c < NMINE * 8; ++c) acc[c] = 0.0f;
     bool pend = false, pend_last = false, pend_live = false;
     float *pend_dst = nullptr;
-    unsigned long long es = 0, ec = 0, ed = 0, ea = 0, ce;
+    unsigned long long es = 0, ec = 0, ed = 0, ea = 0, ce, efirst = 0, eu = 0;
     auto drain = [&]() {  // add a finished TMEM segment, one tile late
       epi_wait(tc::smem_u32(g_full), sc & 1);
       tc::fence_after();
@@ -462,7 +463,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
     for (int k = 0;; ++k) {
+      const unsigned long long cu = prof_clock();
       const int u = take_unit(k, false);
+      eu += prof_clock() - cu;
       if (dyn) {  // one arrival per warp
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&u_empty[k % kUR]), 0));
@@ -489,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc::fence_after();
         const unsigned long long cs = prof_clock();
         es += cs - ce;
+        if (!efirst) efirst = cs - kstart;
         const uint32_t taddr = tmem + lane_off + r * NT + w * 32;
         uint32_t v[32];
         tc::ld32(taddr, v);
@@ -543,6 +547,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (pend) drain();
     if (p.prof && warp == 4 && lane == 0) {
+      p.prof[blockIdx.x * 16 + 12] = efirst;
+      p.prof[blockIdx.x * 16 + 13] = prof_clock() - kstart;
+      p.prof[blockIdx.x * 16 + 15] = eu;
       p.prof[blockIdx.x * 16 + 7] = es;
       p.prof[blockIdx.x * 16 + 8] = ec;
       p.prof[blockIdx.x * 16 + 9] = ea;
