@@ -5,7 +5,7 @@
 //   E = (S + rho)^{-1/2} - rho^{-1/2},
 //   v <- v0;  10 x { y = H v;  est = v.y;  v = y/||y|| };  eta = 1/est.
 //
-// One thread-block cluster of kCluster CTAs per batch element (one ADASAP
+// One thread-block cluster of C CTAs per batch element (one ADASAP
 // iteration of a lookahead batch). CTA c of the cluster owns rows [lo, hi) of
 // K_BB (fp32, the values the tile kernel computes) and of U (fp64); the
 // length-b vector w = P^{-1/2} v is replicated in every CTA's shared memory
@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "../../include/sapgp_b200.h"
@@ -30,7 +31,13 @@ int check_launch(const char *what);
 
 namespace pw {
 
-constexpr int kCluster = 16;  // non-portable cluster size (B200 supports 16)
+// Cluster size per launch (4, 8 or 16 CTAs per batch element): the batch's
+// clusters fill the GPU in ONE wave where they can -- 32 iterations as
+// clusters of 4 (128 CTAs) ran in 1.22 ms against 1.56 ms as 3.5 waves of
+// clusters of 16 -- and a small batch (the ramp's first, whose stepsize the
+// first step waits for) keeps 16 CTAs per iteration for latency.
+// SAP_POWER_CLUSTER forces one size.
+constexpr int kMaxCluster = 16;  // non-portable cluster size (B200 supports 16)
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerPass = 4;  // rows a warp dots at once (amortises w reads)
@@ -75,6 +82,7 @@ __device__ __forceinline__ void block_sum2(double &a, double &c, double *red) {
   }
 }
 
+template <int kCluster>
 __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const int u_smem) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
@@ -205,17 +213,37 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
 #pragma unroll
       for (int rr = 0; rr < kRowsPerPass; ++rr) acc[rr] = 0.0f;
       if (vec4) {
-#pragma unroll 4
-        for (int j = lane * 4; j < b4; j += 128) {
-          const float4 w4 = *reinterpret_cast<const float4 *>(wf + j);
+        // kChunks 128-column chunks of the kRowsPerPass rows are loaded
+        // before any is used: 16 x 16-byte loads in flight per lane (the
+        // compiler otherwise interleaved load and use, leaving the loop
+        // latency-bound on HBM at ~9 B/clk per SM)
+        constexpr int kChunks = 4;
+        const float *krow[kRowsPerPass];
 #pragma unroll
-          for (int rr = 0; rr < kRowsPerPass; ++rr) {
-            const int i = min(i0 + rr, nloc - 1);  // clamped rows are discarded below
-            const float4 kv = *reinterpret_cast<const float4 *>(K + int64_t(lo + i) * a.ldk + j);
-            acc[rr] = fmaf(kv.x, w4.x, acc[rr]);
-            acc[rr] = fmaf(kv.y, w4.y, acc[rr]);
-            acc[rr] = fmaf(kv.z, w4.z, acc[rr]);
-            acc[rr] = fmaf(kv.w, w4.w, acc[rr]);
+        for (int rr = 0; rr < kRowsPerPass; ++rr)
+          krow[rr] = K + int64_t(lo + min(i0 + rr, nloc - 1)) * a.ldk;  // clamped rows discarded below
+        for (int j0 = lane * 4; j0 < b4; j0 += 128 * kChunks) {
+          float4 kv[kChunks][kRowsPerPass];
+#pragma unroll
+          for (int c = 0; c < kChunks; ++c) {
+            const int j = j0 + 128 * c;
+#pragma unroll
+            for (int rr = 0; rr < kRowsPerPass; ++rr)
+              kv[c][rr] = j < b4 ? __ldg(reinterpret_cast<const float4 *>(krow[rr] + j))
+                                 : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          }
+#pragma unroll
+          for (int c = 0; c < kChunks; ++c) {
+            const int j = j0 + 128 * c;
+            if (j >= b4) break;
+            const float4 w4 = *reinterpret_cast<const float4 *>(wf + j);
+#pragma unroll
+            for (int rr = 0; rr < kRowsPerPass; ++rr) {
+              acc[rr] = fmaf(kv[c][rr].x, w4.x, acc[rr]);
+              acc[rr] = fmaf(kv[c][rr].y, w4.y, acc[rr]);
+              acc[rr] = fmaf(kv[c][rr].z, w4.z, acc[rr]);
+              acc[rr] = fmaf(kv[c][rr].w, w4.w, acc[rr]);
+            }
           }
         }
       } else {
@@ -303,7 +331,22 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
   using namespace sap;
   if (b <= 0 || count <= 0 || iters <= 0 || r < 0 || ldk < b || (r && (!U || !E)))
     return fail(SAP_ERR_CONTRACT, "power_stepsize: bad shape b=%d r=%d count=%d", b, r, count);
-  const int per = (b + pw::kCluster - 1) / pw::kCluster;
+  int C = 16;
+  if (const char *e = getenv("SAP_POWER_CLUSTER")) {
+    C = atoi(e);
+  } else {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+        sms = 148;
+    }
+    while (C > 4 && count * C > sms) C /= 2;  // one wave if clusters of >= 4 allow it
+  }
+  if (C != 4 && C != 8 && C != 16)
+    return fail(SAP_ERR_CONTRACT, "power_stepsize: cluster size %d (4, 8 or 16)", C);
+  const int per = (b + C - 1) / C;
   const size_t base = sizeof(double) * (2 * size_t(per) + 2 * size_t(r) + 2 + 2 * pw::kWarps +
                                         pw::kThreads) +
                       sizeof(float) * size_t((b + 3) & ~3);
@@ -314,24 +357,28 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
   const size_t smem = u_smem ? with_u : base;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pw::power_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCap));
-    cudaFuncSetAttribute(pw::power_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(pw::power_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCap));
+    cudaFuncSetAttribute(pw::power_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCap));
+    cudaFuncSetAttribute(pw::power_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCap));
+    cudaFuncSetAttribute(pw::power_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   pw::Args a{Kbb, ldk, strideK, U, strideU, E, rho, v0, b, r, iters, lam, eta, bad};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(count * pw::kCluster));
+  cfg.gridDim = dim3(unsigned(count * C));
   cfg.blockDim = dim3(pw::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pw::kCluster;
+  at[0].val.clusterDim.x = unsigned(C);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, pw::power_kernel, a, u_smem);
+  const cudaError_t e = C == 4 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<4>, a, u_smem)
+                        : C == 8 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<8>, a, u_smem)
+                                 : cudaLaunchKernelEx(&cfg, pw::power_kernel<16>, a, u_smem);
   if (e != cudaSuccess) return fail(SAP_ERR_DEVICE, "power_kernel: %s", cudaGetErrorString(e));
   return check_launch("power_kernel");
 }
