@@ -184,7 +184,7 @@ class Lookahead:
         # at lookahead depth 4); its kernels are short, so they slip in between
         # two block products. SAP_FAST_STREAM=0 keeps it on the solver's stream.
         if os.environ.get("SAP_FAST_STREAM", "1") == "1":
-            self.fast = torch.cuda.Stream(device=dev, priority=-1)
+            self.fast = torch.cuda.Stream(device=dev, priority=int(os.environ.get("SAP_FAST_PRIORITY", "-1")))
         else:
             self.fast = None
         self.tcp = tcp
