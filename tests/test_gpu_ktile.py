@@ -2,7 +2,9 @@
 input) against the per-block tile kernel sap_ktile_f32: same values bit for
 bit, one launch per batch. Both are checked against the CPU oracle's
 block_block (KernelOracle.block, kernels.py:129-136) at the headline shape in
-tests/test_gpu_config3.py::test_hot_path_kbb_tile_matches_oracle."""
+tests/test_gpu_config3.py::test_hot_path_kbb_tile_matches_oracle. The power
+iteration that consumes those tiles (sap_power_stepsize) is checked for each
+cluster size it launches with against a torch fp64 restatement."""
 import numpy as np
 import pytest
 
@@ -39,3 +41,49 @@ def test_ktile_batch_bitwise(family, b, d):
     torch.cuda.synchronize()
     assert torch.equal(ref, got)
     assert torch.equal(got[:, :, :b], got[:, :, :b].transpose(1, 2))  # symmetric
+
+
+@pytest.mark.parametrize("cluster", ["4", "8", "16", None])
+@pytest.mark.parametrize("count,b,r", [(32, 2000, 100), (5, 1000, 100), (3, 130, 7), (2, 64, 0)])
+def test_power_stepsize_cluster_sizes(cluster, count, b, r, monkeypatch):
+    """sap_power_stepsize (csrc/power.cu; randnla.py:165-196) for every cluster
+    size the launcher picks (None: its own choice, one wave when it can)
+    against the same preconditioned power iteration in torch fp64."""
+    if cluster is None:
+        monkeypatch.delenv("SAP_POWER_CLUSTER", raising=False)
+    else:
+        monkeypatch.setenv("SAP_POWER_CLUSTER", cluster)
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(count * b + r)
+    A = torch.randn(count, b, b, device=dev, generator=g) / b
+    Kbb = (A @ A.transpose(1, 2)).float().contiguous()
+    rho = torch.full((count,), 0.5, device=dev, dtype=torch.float64)
+    if r:
+        U = torch.linalg.qr(torch.randn(count, b, r, device=dev, dtype=torch.float64,
+                                        generator=g))[0].contiguous()
+        S = torch.rand(count, r, device=dev, dtype=torch.float64, generator=g) * 10
+        E = (1 / torch.sqrt(S + rho[:, None]) - 1 / torch.sqrt(rho[:, None])).contiguous()
+    else:
+        U, E = None, torch.zeros((count, 1), device=dev, dtype=torch.float64)
+    v0 = torch.randn(count, b, device=dev, dtype=torch.float64, generator=g)
+    v0 /= v0.norm(dim=1, keepdim=True)
+    eta = torch.empty(count, device=dev, dtype=torch.float64)
+    bad = torch.zeros(count, device=dev, dtype=torch.int32)
+    K.power_stepsize(Kbb, U, E, rho, v0, 1e-2, 10, eta, bad)
+
+    def Pd(x):  # P^{-1/2} x
+        y = x * rho.rsqrt()[:, None]
+        if r:
+            y = y + torch.bmm(U, (E * torch.bmm(U.transpose(1, 2), x[:, :, None])[:, :, 0])
+                              [:, :, None])[:, :, 0]
+        return y
+
+    v, Kd = v0.clone(), Kbb.double()
+    for _ in range(10):
+        w = Pd(v)
+        y = Pd(torch.bmm(Kd, w[:, :, None])[:, :, 0] + 1e-2 * w)
+        est = (v * y).sum(1)
+        v = y / y.norm(dim=1, keepdim=True)
+    torch.cuda.synchronize()
+    assert int(bad.abs().sum()) == 0
+    assert torch.allclose(eta, 1 / est, rtol=1e-7, atol=0)
