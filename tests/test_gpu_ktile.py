@@ -40,11 +40,14 @@ def test_ktile_batch_bitwise(family, b, d):
     K.ktile_f32_batch(spec, Xb, rsq, pts.d, got)
     torch.cuda.synchronize()
     assert torch.equal(ref, got)
+    # exactly symmetric (the power iteration reads one triangle of it)
+    assert torch.equal(got[:, :, :b], got[:, :, :b].transpose(1, 2))
     assert torch.equal(got[:, :, :b], got[:, :, :b].transpose(1, 2))  # symmetric
 
 
 @pytest.mark.parametrize("cluster", ["4", "8", "16", None])
-@pytest.mark.parametrize("count,b,r", [(32, 2000, 100), (5, 1000, 100), (3, 130, 7), (2, 64, 0)])
+@pytest.mark.parametrize("count,b,r", [(32, 2000, 100), (5, 1000, 100), (3, 130, 7), (2, 64, 0),
+                                       (2, 333, 5)])
 def test_power_stepsize_cluster_sizes(cluster, count, b, r, monkeypatch):
     """sap_power_stepsize (csrc/power.cu; randnla.py:165-196) for every cluster
     size the launcher picks (None: its own choice, one wave when it can)
@@ -56,7 +59,8 @@ def test_power_stepsize_cluster_sizes(cluster, count, b, r, monkeypatch):
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev).manual_seed(count * b + r)
     A = torch.randn(count, b, b, device=dev, generator=g) / b
-    Kbb = (A @ A.transpose(1, 2)).float().contiguous()
+    Kbb = (A @ A.transpose(1, 2)).float()
+    Kbb = (0.5 * (Kbb + Kbb.transpose(1, 2))).contiguous()  # exactly symmetric, as K_BB
     rho = torch.full((count,), 0.5, device=dev, dtype=torch.float64)
     if r:
         U = torch.linalg.qr(torch.randn(count, b, r, device=dev, dtype=torch.float64,
