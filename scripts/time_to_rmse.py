@@ -45,7 +45,7 @@ yt = prob.ytest
 
 
 def test_rmse(eng):
-    W = eng.materialize("W")[:, :1].contiguous()          # posterior-mean weights
+    W = eng.materialize("W", col=0)                       # posterior-mean weights only
     mean = o.cross_matmul(Xt, W)[:, 0].double().cpu().numpy()
     return float(np.sqrt(np.mean((mean - yt) ** 2)))
 
@@ -54,11 +54,15 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 eng = AdasapEngine(o, prob.Y, cfg, sap.resolve_accel(cfg, n, b), total=total)
 traj = []
+ev_s = 0.0  # time spent in the RMSE evaluations (excluded from solve_seconds)
 for t in range(total):
     eng.step()
     if (t + 1) % a.every == 0 or t + 1 == total:
         torch.cuda.synchronize()
-        traj.append((t + 1, time.perf_counter() - t0, test_rmse(eng)))
+        now = time.perf_counter()
+        rm = test_rmse(eng)
+        traj.append((t + 1, now - t0 - ev_s, rm))
+        ev_s += time.perf_counter() - now
 eng.la.check_flags()
 eng.close()
 final = traj[-1][2]
@@ -75,9 +79,10 @@ out = {"workload": f"synthetic {a.family} GP n={n} d={d} b={b} m={m} r={r}",
        "target": f"test RMSE after {a.passes} passes", "final_test_rmse": final,
        "noise_level_sqrt_lam_over_std": float(np.sqrt(prob.lam) / np.std(prob.y)),
        "within_1pct": first_within(1e-2), "within_0.1pct": first_within(1e-3),
-       "total_seconds": traj[-1][1], "iterations": total,
-       "seconds_include": "setup of the engine (lookahead start), every solver step, and the "
-                          "RMSE evaluations (materialise W + cross product + readback)",
+       "total_seconds": traj[-1][1], "iterations": total, "evaluation_seconds_excluded": ev_s,
+       "seconds_include": "setup of the engine (lookahead start) and every solver step; the "
+                          "RMSE evaluations (one column of W materialised, the tensor-core "
+                          "cross product, readback) are timed separately and excluded",
        "trajectory": [{"iterations": it, "seconds": round(sec, 4), "rmse": rm}
                       for it, sec, rm in traj]}
 print(json.dumps(out))
