@@ -29,6 +29,7 @@ restatement of the reference) timed on this host's cores for one iteration.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -221,6 +222,13 @@ def run_b200(args):
                                   seed=CONFIG["seed"], lam=CONFIG["lam"], device=dev)
     spec = prob.spec()
     oracle = sap.KernelOracle(spec, prob.X, prob.lam, device=dev)
+    # Python's full (generation-2) collections scan every tracked object --
+    # ~180k after importing torch, ~37 ms per collection -- holding the GIL, so
+    # the lookahead's producers stall at random steps (e2e runs of 0.1-0.5 s
+    # instead of ~0.09 s). Objects alive now (modules, the problem) are frozen
+    # out of those scans, as a long-running service would do after start-up
+    # (scripts/e2e_phases.py GC=on/off/freeze/check).
+    gc.freeze()
     warm = max(args.warmup, RAMP_ITERS)
     cfg = sap.RunConfig(lam=prob.lam, blocksize=CONFIG["b"], nystrom_rank=CONFIG["r"],
                         residual_every=0, seed=CONFIG["seed"])
@@ -435,7 +443,7 @@ def run_e2e(args, prob, spec, dev):
                       "each step's stepsize read to the host, + state.W (final iterate to "
                       "host float64); setup and readback inside the timed region",
             "seconds": med, "runs_seconds": [round(r, 4) for r in runs],
-            "statistic": f"median of {E2E_RUNS} timed runs",
+            "statistic": f"median of {E2E_RUNS} timed runs (gc.freeze() after setup)",
             "solve": {"iters_per_s": K / (t3 - t2), "seconds": t3 - t2,
                       "final_residual": res.trace.final_residual(),
                       "note": f"adasap_solve(max_iters={K}) from host X/Y to host W, including "

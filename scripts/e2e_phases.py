@@ -10,7 +10,13 @@ n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
 prob = synthetic.make_problem(n, d, "matern32", m, seed=0, lam=1e-2, device="cuda")
 X, Y = np.ascontiguousarray(prob.X), np.ascontiguousarray(prob.Y)
 cfg = sap.RunConfig(lam=1e-2, blocksize=b, nystrom_rank=r, residual_every=0, seed=0)
-for rep in range(8):
+if os.environ.get("GC") == "freeze":  # diagnosis: full collections over the imported modules
+    import gc
+    gc.freeze()
+elif os.environ.get("GC") in ("off", "check"):
+    import gc
+    gc.disable()
+for rep in range(int(os.environ.get("REPS", "8"))):
     torch.cuda.synchronize()
     T = [time.perf_counter()]
     o = sap.KernelOracle(prob.spec(), X, 1e-2, device="cuda"); torch.cuda.synchronize(); T.append(time.perf_counter())
@@ -39,5 +45,18 @@ for rep in range(8):
     W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
     st.iteration = st.iteration; T.append(time.perf_counter())
     names = ["oracle", "bind+step0", "19 steps", "W readback", "close"]
+    if os.environ.get("GC") == "check":  # what one rep leaves to the cyclic collector
+        import gc
+        del st, W
+        gc.set_debug(gc.DEBUG_SAVEALL)
+        g0 = time.perf_counter()
+        found = gc.collect()
+        dt_gc = 1e3 * (time.perf_counter() - g0)
+        import collections
+        kinds = collections.Counter(type(x).__qualname__ for x in gc.garbage).most_common(8)
+        gc.garbage.clear()
+        gc.set_debug(0)
+        print(f"   gc.collect: {found} unreachable objects in {dt_gc:.1f} ms; tracked objects "
+              f"{len(gc.get_objects())}; kinds {kinds}", flush=True)
     print(rep, "  ".join(f"{k} {1e3*(T[i+1]-T[i]):.1f} ms" for i, k in enumerate(names)),
           "slow steps (host ms):", slow, flush=True)

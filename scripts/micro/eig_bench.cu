@@ -5,6 +5,12 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <chrono>
+__global__ void spin(unsigned long long ns) {
+  const unsigned long long t0 = clock64();
+  while (clock64() - t0 < ns * 2) {
+  }
+}
 extern "C" int sap_sym_eig_batch(double *, int64_t, int, int, int, double *, double *, int64_t, int,
                                  int, int *, void *, size_t, void *);
 int main(int argc, char **argv) {
@@ -43,6 +49,20 @@ int main(int argc, char **argv) {
                                     bh.data(), wh, info, count);
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("cusolverDnXsyevBatched r=%d count=%d: %.3f ms (status %d, ws %zu)\n", r, count, ms, st, wd);
+  }
+  // does the call block the host until the work queued before it finishes?
+  // (a 20 ms spin kernel ahead of it on the same stream)
+  printf("host workspace %zu bytes\n", wh);
+  for (int it = 0; it < 2; ++it) {
+    cudaMemcpy(dA, dB, h.size() * 8, cudaMemcpyDeviceToDevice);
+    cudaDeviceSynchronize();
+    spin<<<1, 32>>>(20000000ull);
+    auto h0 = std::chrono::steady_clock::now();
+    cusolverDnXsyevBatched(H, P, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, r, CUDA_R_64F,
+                           dA, r, CUDA_R_64F, dW, CUDA_R_64F, bd, wd, bh.data(), wh, info, count);
+    const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    cudaDeviceSynchronize();
+    printf("cusolverDnXsyevBatched host time behind a 20 ms kernel: %.2f ms\n", hms);
   }
   for (int it = 0; it < 3; ++it) {
     cudaMemcpy(dA, dB, h.size() * 8, cudaMemcpyDeviceToDevice);
