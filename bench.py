@@ -416,6 +416,10 @@ def run_e2e(args, prob, spec, dev):
     # 0.1-0.5 s on the host (seen in every phase on some boxes, GPU idle;
     # scripts/e2e_phases.py), which one run would report as the throughput
     runs, finite = [], True
+    gc_log = []
+    if xfer.TRACE is not None:  # SAP_TRACE=1 (diagnosis): garbage collections during the runs
+        gc.callbacks.append(lambda phase, info: gc_log.append(
+            (time.perf_counter(), phase, info.get("generation"))))
     for _ in range(E2E_RUNS):
         torch.cuda.synchronize()
         x0 = xfer.snapshot()
@@ -427,6 +431,24 @@ def run_e2e(args, prob, spec, dev):
         st._e.close()  # after the timed region: the lookahead's producers run ahead
         st.iteration = st.iteration  # detach: releases the engine
         runs.append(t1 - t0)
+        if xfer.TRACE is not None:  # SAP_TRACE=1 (diagnosis): the run's marks, gaps > 10 ms
+            last = t0
+            for tt, th, tag in xfer.TRACE:
+                if t0 <= tt <= t1 and tt - last > 0.01:
+                    print(f"# e2e run {len(runs)} ({1e3 * (t1 - t0):.0f} ms): "
+                          f"{1e3 * (tt - t0):7.1f} ms {th} {tag} after a {1e3 * (tt - last):.0f} ms gap",
+                          file=sys.stderr)
+                last = max(last, tt)
+            xfer.TRACE.clear()
+            starts = {}
+            for tt, phase, gen in gc_log:
+                if phase == "start":
+                    starts[gen] = tt
+                elif gen in starts and t0 <= tt <= t1 and tt - starts[gen] > 0.002:
+                    print(f"# e2e run {len(runs)}: gc generation {gen} at "
+                          f"{1e3 * (starts[gen] - t0):.1f} ms took {1e3 * (tt - starts[gen]):.1f} ms",
+                          file=sys.stderr)
+            gc_log.clear()
         finite = finite and bool(np.isfinite(W).all() and np.isfinite(etas).all())
         del W
     h2d, d2h = x1["h2d"] - x0["h2d"], x1["d2h"] - x0["d2h"]

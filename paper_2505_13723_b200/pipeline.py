@@ -190,8 +190,10 @@ class Lookahead:
         self.tcp = tcp
         ka = tcp.ka if tcp is not None else 0
         fdt = tcp.dtype if tcp is not None else torch.float32
+        xfer.mark("lookahead: streams")
         self.slots = [_Slot(self.L, b, self.r, oracle.points.ldx, dev, ka, fdt)
                       for _ in range(self.nslots)]
+        xfer.mark("lookahead: slots")
         # per-slot scratch of the tensor-core sketch (used one plan at a time by
         # the slot's producer)
         # (only for blocks of >= 512 points: below that the 256-row tiles are
@@ -218,6 +220,7 @@ class Lookahead:
                 _l, _ = torch.linalg.cholesky_ex(_a)
                 torch.cholesky_inverse(_l)
                 torch.linalg.solve_triangular(_l, _a, upper=False)
+            xfer.mark("lookahead: linalg init")
         # batch k covers iterations [bounds[k], bounds[k+1]); sizes ramp 1, 4,
         # 16, ... up to L, extended on demand (_has_batch). Growth 4 rather
         # than 2: a batch's host-side cost is mostly per batch, not per
