@@ -422,6 +422,8 @@ def run_e2e(args, prob, spec, dev):
             (time.perf_counter(), phase, info.get("generation"))))
     for _ in range(E2E_RUNS):
         torch.cuda.synchronize()
+        if xfer.TRACE is not None:
+            m0 = torch.cuda.memory_stats()
         x0 = xfer.snapshot()
         t0 = time.perf_counter()
         W, etas, st = step_run(K)
@@ -449,6 +451,11 @@ def run_e2e(args, prob, spec, dev):
                           f"{1e3 * (starts[gen] - t0):.1f} ms took {1e3 * (tt - starts[gen]):.1f} ms",
                           file=sys.stderr)
             gc_log.clear()
+            m1 = torch.cuda.memory_stats()
+            print(f"# e2e run {len(runs)}: cudaMalloc {m1.get('num_device_alloc', 0) - m0.get('num_device_alloc', 0)}"
+                  f", cudaFree {m1.get('num_device_free', 0) - m0.get('num_device_free', 0)}, "
+                  f"alloc retries {m1.get('num_alloc_retries', 0) - m0.get('num_alloc_retries', 0)}",
+                  file=sys.stderr)
         finite = finite and bool(np.isfinite(W).all() and np.isfinite(etas).all())
         del W
     h2d, d2h = x1["h2d"] - x0["h2d"], x1["d2h"] - x0["d2h"]

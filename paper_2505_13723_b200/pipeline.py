@@ -72,6 +72,24 @@ class IterPlan:
     batch_eta: torch.Tensor | None = None  # the batch's stepsizes (device)
 
 
+# One production stream per (device, priority) for the whole process, reused
+# by every engine: the caching allocator keeps freed blocks in the pool of the
+# stream they were allocated on, so a fresh stream per engine made every new
+# engine's production allocate (cudaMalloc, ~15 segments) instead of reusing
+# the previous engine's blocks, and stalled the first steps after each bind.
+_FAST_STREAMS = {}
+_FAST_LOCK = threading.Lock()
+
+
+def _fast_stream(dev, priority):
+    key = (torch.device(dev).index, priority)
+    with _FAST_LOCK:
+        st = _FAST_STREAMS.get(key)
+        if st is None:
+            st = _FAST_STREAMS[key] = torch.cuda.Stream(device=dev, priority=priority)
+        return st
+
+
 class _Slot:
     def __init__(self, L, b, r, ldx, dev, ka=0, fdtype=torch.float32):
         f32, f64, i64 = torch.float32, torch.float64, torch.int64
@@ -184,7 +202,7 @@ class Lookahead:
         # at lookahead depth 4); its kernels are short, so they slip in between
         # two block products. SAP_FAST_STREAM=0 keeps it on the solver's stream.
         if os.environ.get("SAP_FAST_STREAM", "1") == "1":
-            self.fast = torch.cuda.Stream(device=dev, priority=int(os.environ.get("SAP_FAST_PRIORITY", "-1")))
+            self.fast = _fast_stream(dev, int(os.environ.get("SAP_FAST_PRIORITY", "-1")))
         else:
             self.fast = None
         self.tcp = tcp

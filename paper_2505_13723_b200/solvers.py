@@ -524,7 +524,11 @@ class AdasapEngine:
         # (double buffering; skipped when the state would not fit beside it)
         self.zop_next = None
         if self.fused and self.use_tc:
-            free, _ = torch.cuda.mem_get_info(self.dev)
+            # room left for this process's allocations (the allocator's own
+            # counters: cudaMemGetInfo, a driver call, cost up to ~40 ms per
+            # bind next to the lookahead's producers)
+            free = torch.cuda.get_device_properties(self.dev).total_memory - \
+                torch.cuda.memory_allocated(self.dev)
             if free > 2 * self.zop.hi.numel() * 2 + (4 << 30):
                 self.zop_next = ZOperand(m, nl, self.dev)
         xfer.mark("bind: buffers")
