@@ -106,31 +106,77 @@ struct Next {
 };
 
 // Part `part` of `parts` of the whole pass, with `nthr` cooperating threads
-// (thread `tid`): contiguous point ranges per part so the loads stream.
+// (thread `tid`): contiguous point ranges per part so the loads stream. Short
+// columns per part (config 2: ~84 8-point groups) make the part's (column,
+// group) items one flat index space, groups fastest, two items in flight per
+// thread (the control warps hold 64 registers): a column-at-a-time loop left
+// the pass latency-bound there and longer than the block-row product it hides
+// under (config 2: 3860 -> 4470 iterations/s).
 __device__ __forceinline__ void next_pass(const Next &zn, int part, int parts, int tid, int nthr) {
   const int64_t groups = zn.ldz / 8;
   const int64_t g0 = groups * part / parts, g1 = groups * (part + 1) / parts;
-  for (int c = 0; c < zn.m; ++c) {
-    const float sc = scale(zn.zp, zn.zq, zn.Pb, zn.Qb, zn.Q != nullptr, c);
-    if (part == 0 && tid == 0) zn.zscale[c] = sc;
-    const float a = zn.zp * sc, bq = zn.zq * sc;
-    const float *pr = zn.P + int64_t(c) * zn.ldp;
-    const float *qr = zn.Q ? zn.Q + int64_t(c) * zn.ldp : nullptr;
-    __half *hr = zn.Zhi + int64_t(c) * zn.ldz, *lr = zn.Zlo + int64_t(c) * zn.ldz;
-    int64_t g = g0 + tid;
-    // two groups per step: 64 bytes of P and Q loads in flight per thread
-    for (; g + nthr < g1; g += 2 * nthr) {
-      float z0[8], z1[8];
-      load8<true>(pr, qr, g * 8, zn.n, a, bq, z0);
-      load8<true>(pr, qr, (g + nthr) * 8, zn.n, a, bq, z1);
-      store8<true>(z0, hr, lr, g * 8);
-      store8<true>(z1, hr, lr, (g + nthr) * 8);
+  const unsigned ng = unsigned(g1 - g0);
+  const bool hasq = zn.Q != nullptr;
+  if (part == 0)
+    for (int c = tid; c < zn.m; c += nthr) zn.zscale[c] = scale(zn.zp, zn.zq, zn.Pb, zn.Qb, hasq, c);
+  if (ng == 0) return;
+  if (ng >= 4u * unsigned(nthr)) {
+    // long columns (config 3: ~845 groups per part): column at a time, which
+    // measured faster there than the flat loop below (its index arithmetic
+    // and deeper memory pressure cost the RBF block product 11%)
+    for (int c = 0; c < zn.m; ++c) {
+      const float sc = scale(zn.zp, zn.zq, zn.Pb, zn.Qb, hasq, c);
+      const float ca = zn.zp * sc, cb = zn.zq * sc;
+      const float *pr = zn.P + int64_t(c) * zn.ldp;
+      const float *qr = hasq ? zn.Q + int64_t(c) * zn.ldp : nullptr;
+      __half *hr = zn.Zhi + int64_t(c) * zn.ldz, *lr = zn.Zlo + int64_t(c) * zn.ldz;
+      int64_t g = g0 + tid;
+      for (; g + nthr < g1; g += 2 * nthr) {  // two groups per step: 64 B of loads in flight
+        float z0[8], z1[8];
+        load8<true>(pr, qr, g * 8, zn.n, ca, cb, z0);
+        load8<true>(pr, qr, (g + nthr) * 8, zn.n, ca, cb, z1);
+        store8<true>(z0, hr, lr, g * 8);
+        store8<true>(z1, hr, lr, (g + nthr) * 8);
+      }
+      if (g < g1) {
+        float z0[8];
+        load8<true>(pr, qr, g * 8, zn.n, ca, cb, z0);
+        store8<true>(z0, hr, lr, g * 8);
+      }
     }
-    if (g < g1) {
-      float z0[8];
-      load8<true>(pr, qr, g * 8, zn.n, a, bq, z0);
-      store8<true>(z0, hr, lr, g * 8);
+    return;
+  }
+  const unsigned total = ng * unsigned(zn.m);
+  constexpr int kD = 2;
+  int cur = -1;
+  float a = 0.0f, bq = 0.0f;
+  for (unsigned base = unsigned(tid); base < total; base += kD * unsigned(nthr)) {
+    float z[kD][8];
+    int cc[kD];
+    int64_t jj[kD];
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+      const unsigned it = base + unsigned(u * nthr);
+      cc[u] = -1;
+      if (it < total) {
+        const int c = int(it / ng);
+        if (c != cur) {
+          const float sc = scale(zn.zp, zn.zq, zn.Pb, zn.Qb, hasq, c);
+          a = zn.zp * sc;
+          bq = zn.zq * sc;
+          cur = c;
+        }
+        cc[u] = c;
+        jj[u] = (g0 + int64_t(it - unsigned(c) * ng)) * 8;
+        load8<true>(zn.P + int64_t(c) * zn.ldp, hasq ? zn.Q + int64_t(c) * zn.ldp : nullptr,
+                    jj[u], zn.n, a, bq, z[u]);
+      }
     }
+#pragma unroll
+    for (int u = 0; u < kD; ++u)
+      if (cc[u] >= 0)
+        store8<true>(z[u], zn.Zhi + int64_t(cc[u]) * zn.ldz, zn.Zlo + int64_t(cc[u]) * zn.ldz,
+                     jj[u]);
   }
 }
 
