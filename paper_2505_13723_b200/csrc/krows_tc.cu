@@ -473,8 +473,23 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
   }
   // the next operand inside the CTA-pair kernel (16-byte vector rows only)
   auto al16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  // ... and only when the two control warps finish it under the product: the
+  // pass moves 12 n m bytes at ~0.9 TB/s over the GPU (long columns per CTA)
+  // or ~0.5 TB/s (short ones, zop::next_pass), the product takes ~b n /
+  // (1.4e12 Matern, 2.2e12 RBF/cosine entries/s). Otherwise the separate pass
+  // (full HBM bandwidth, ~13 us at config 2) is cheaper than a side job the
+  // launch waits for (config 2: side job 0.151 ms launch vs ~0.12 + 0.013).
+  // SAP_ZNEXT_SEPARATE=1 / SAP_ZNEXT_SIDE=1 force either.
+  bool side_fits = true;
+  if (!getenv("SAP_ZNEXT_SIDE")) {
+    const double rate = family == SAP_MATERN32 || family == SAP_MATERN52 ? 1.4e12 : 2.2e12;
+    const bool short_cols = (ldz / 8) / kSms < 4 * 64;
+    const double side_s = 12.0 * double(ncols) * double(m) / (short_cols ? 0.5e12 : 0.9e12);
+    const double prod_s = double(bpad) * double(ncols) / rate;
+    side_fits = side_s < 0.95 * prod_s;
+  }
   const bool side = Zhi_next && pair && ldp % 4 == 0 && ldz % 8 == 0 && al16(P) &&
-                    (!Q || al16(Q)) && al16(Zhi_next) && al16(Zlo_next) &&
+                    (!Q || al16(Q)) && al16(Zhi_next) && al16(Zlo_next) && side_fits &&
                     getenv("SAP_ZNEXT_SEPARATE") == nullptr;
   if (side)
     p.zn = zop::Next{P, Q, ldp, ncols, m, float(zp), float(zq), Pb, Qb,
