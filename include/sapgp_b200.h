@@ -58,6 +58,7 @@ enum { SAP_RBF = 0, SAP_MATERN32 = 1, SAP_MATERN52 = 2 };
  * value is cos(x . F_k + p_k) instead of k(x, y); sap_krows_tc only */
 enum { SAP_COSINE = 3 };
 #define SAP_TC_KA_F16 48
+#define SAP_TC_KA_F16X64 96
 
 int sap_abi_version(void);
 const char *sap_last_error(void);
@@ -217,9 +218,10 @@ int sap_tc_supported(int d, int m);
  * Tensor-core block-row product (tcgen05 + TMEM + TMA, sm_100a):
  * out[i, c] (=, or +=) variance * sum_j k(row_i, col_j) Z[j, c] with rows
  * RAg ([bpad][ka], bpad a multiple of 128), columns CA ([ncols][ka]) and Z
- * (features fp32 for ka = 32 or 64; ka = SAP_TC_KA_F16 means 32 fp16
- * features per point -- the same tf32-rounded values, exact in fp16 -- and
- * needs bpad a multiple of 256; the distance GEMM then runs kind::f16)
+ * (features fp32 for ka = 32 or 64; ka = SAP_TC_KA_F16 / SAP_TC_KA_F16X64
+ * means 32 / 64 fp16 features per point -- the same tf32-rounded values,
+ * exact in fp16 -- and needs bpad a multiple of 256; the distance GEMM then
+ * runs kind::f16)
  * given by sap_z_operand. Diagonal rule as sap_krows_times (row_ids vs
  * col_base + j). nz <= 128.
  */

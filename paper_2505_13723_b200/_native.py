@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("SAP_LIB_PATH") or os.path.join(
 
 SAP_OK, SAP_ERR_CONTRACT, SAP_ERR_NUMERICAL, SAP_ERR_DEVICE = 0, 1, 2, 3
 SAP_TC_KA_F16 = 48  # include/sapgp_b200.h: 32 fp16 features per point
+SAP_TC_KA_F16X64 = 96  # 64 fp16 features per point
 FAMILY_CODES = {"rbf": 0, "matern32": 1, "matern52": 2}
 ABI_VERSION = 1
 

@@ -424,7 +424,8 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
                       const float *Q, int64_t ldp, double zp, double zq, const float *Pb,
                       const float *Qb, void *Zhi_next, void *Zlo_next, float *zscale_next,
                       void *stream) {
-  const bool half = ka == tck2::kKaF16;  // 32 fp16 features per point
+  const bool half = ka == tck2::kKaF16 || ka == tck2::kKaF16x64;  // 32 / 64 fp16 features
+  const int kah = ka == tck2::kKaF16x64 ? 64 : 32;                 // their count
   if (b <= 0 || m <= 0 || ncols <= 0 || (ka != 32 && ka != 64 && !half) || nz % 16 || nz < m ||
       nz > 128 || bpad % BM || bpad < b || ldz % 8 || ldz < ncols || ncols > INT32_MAX)
     return fail(SAP_ERR_CONTRACT, "krows_tc: bad shape b=%lld m=%d nz=%d ncols=%lld ka=%d",
@@ -505,10 +506,11 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
   const uint32_t zbox = pair ? nz / 2 : nz;
   CUtensorMap tm_rows, tm_cols, tm_zhi, tm_zlo;
   const bool fmaps_ok =
-      half ? make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, RAg, 32, bpad, 64, 32, BM,
-                      CU_TENSOR_MAP_SWIZZLE_64B) &&
-                 make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, CA, 32, ncols, 64, 32, xbox,
-                          CU_TENSOR_MAP_SWIZZLE_64B)
+      half ? make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, RAg, kah, bpad, size_t(kah) * 2,
+                      kah, BM, kah == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) &&
+                 make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, CA, kah, ncols,
+                          size_t(kah) * 2, kah, xbox,
+                          kah == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B)
            : make_map(&tm_rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, RAg, ka, bpad, size_t(ka) * 4, 32,
                       BM) &&
                  make_map(&tm_cols, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CA, ka, ncols,

@@ -102,7 +102,7 @@ struct Geometry2 {
   static constexpr uint32_t STAGES = stages_raw > 8 ? 8 : stages_raw;
   static constexpr uint32_t smem = fixed + STAGES * stage_bytes;
   static constexpr bool fits = STAGES >= 3 && NZ % 16 == 0 && NZ >= 16 && kGCol + NZ <= 512 &&
-                              (!H || KA == 32);
+                              (!H || KA == 32 || KA == 64);
 };
 
 // K-major SWIZZLE_64B descriptor (fp16 features: 64-byte rows, 8-row atoms of
@@ -118,7 +118,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_zlo, const Params p) {
   using Geo = Geometry2<NZ, KA, H>;
   constexpr uint32_t STAGES = Geo::STAGES;
-  constexpr int KATOMS = H ? 1 : KA / 32;  // 128-byte (fp32) or one 64-byte (fp16) atom
+  // 128-byte fp32 atoms, or one fp16 atom: 64-byte rows (32 features) or
+  // 128-byte rows (64 features)
+  constexpr int KATOMS = H ? 1 : KA / 32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -285,8 +287,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t full0 = tc::smem_u32(full), empty0 = tc::smem_u32(empty);
       const uint32_t sfull0 = tc::smem_u32(s_full), pfull0 = tc::smem_u32(p_full);
       const uint64_t stage_desc0 = kDescBase | (tc::smem_u32(sStage) >> 4);
-      const uint64_t f_desc0 = (H ? kDescBase64 : kDescBase) | (tc::smem_u32(sStage) >> 4);
-      const uint64_t a_desc0 = (H ? kDescBase64 : kDescBase) | (tc::smem_u32(sA) >> 4);
+      constexpr uint64_t kFDesc = (H && KA == 32) ? kDescBase64 : kDescBase;
+      const uint64_t f_desc0 = kFDesc | (tc::smem_u32(sStage) >> 4);
+      const uint64_t a_desc0 = kFDesc | (tc::smem_u32(sA) >> 4);
       uint32_t s1 = 0, ph1 = 0, r1 = 0;    // GEMM1 cursor (one tile ahead)
       uint32_t s2 = 0, r2 = 0, ph2 = 0;    // GEMM2 cursor
       uint32_t sc = 0;
@@ -581,6 +584,7 @@ bool launch_tc2_shape(const CUtensorMap &a, const CUtensorMap &c, const CUtensor
 
 // ka: 32 / 64 fp32 features, or kKaF16 (32 fp16 features, include/sapgp_b200.h)
 constexpr int kKaF16 = SAP_TC_KA_F16;
+constexpr int kKaF16x64 = SAP_TC_KA_F16X64;
 template <int FAM>
 bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtensorMap &zh,
                        const CUtensorMap &zl, const Params &p, int nz, int ka, int grid,
@@ -589,6 +593,7 @@ bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtenso
   return ka == 32     ? launch_tc2_shape<FAM, NZV, 32, false>(a, c, zh, zl, p, grid, st)  \
          : ka == 64   ? launch_tc2_shape<FAM, NZV, 64, false>(a, c, zh, zl, p, grid, st)  \
          : ka == kKaF16 ? launch_tc2_shape<FAM, NZV, 32, true>(a, c, zh, zl, p, grid, st) \
+         : ka == kKaF16x64 ? launch_tc2_shape<FAM, NZV, 64, true>(a, c, zh, zl, p, grid, st) \
                         : false;
   switch (nz) {
     case 16: SAP_TC2_KA(16)
@@ -605,8 +610,8 @@ bool launch_tc2_family(const CUtensorMap &a, const CUtensorMap &c, const CUtenso
 }
 
 inline bool tc2_fits(int nz, int ka) {
-  const bool h = ka == kKaF16;
-  if (h) ka = 32;
+  const bool h = ka == kKaF16 || ka == kKaF16x64;
+  if (h) ka = ka == kKaF16 ? 32 : 64;
   if (nz % 16 || nz < 16 || kGCol + nz > 512 || (ka != 32 && ka != 64)) return false;
   const uint32_t elem = h ? 2 : 4;
   const uint32_t stage = (NT / 2) * ka * elem + 2 * 2 * (nz / 2) * 128;

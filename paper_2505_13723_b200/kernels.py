@@ -176,11 +176,13 @@ class TcPoints:
         # the features are tf32-rounded splits, so the fp16 copy is exact while
         # every magnitude stays inside fp16's range (|z|^2 < 2^14 leaves room
         # for the -2 z column form); SAP_TC_F16=0 keeps fp32
+        # (d >= 10 needs 64 features: fp16 too, 128-byte rows, since round 2)
         self.half = False
-        if self.ka == 32 and os.environ.get("SAP_TC_F16", "1") == "1":
+        if os.environ.get("SAP_TC_F16", "1") == "1":
             zmax2 = _CFAM[spec.family] * float(((Xd * inv) ** 2).sum(1).max())
             self.half = zmax2 < 2.0 ** 14
-        self.ka_code = nat.SAP_TC_KA_F16 if self.half else self.ka
+        self.ka_code = ((nat.SAP_TC_KA_F16 if self.ka == 32 else nat.SAP_TC_KA_F16X64)
+                        if self.half else self.ka)
         self.dtype = torch.float16 if self.half else torch.float32
         if self.half:
             self.CA = self.CA.half()

@@ -235,13 +235,15 @@ def test_cross_matmul_tensor_path_matches_oracle(fam):
     assert rel(got, ref) < 1e-4
 
 
+@pytest.mark.parametrize("d", [9, 11, 14])
 @pytest.mark.parametrize("fam", FAMILIES)
-def test_fp16_and_fp32_feature_paths_agree(fam, monkeypatch):
+def test_fp16_and_fp32_feature_paths_agree(fam, d, monkeypatch):
     """The distance GEMM on fp16 features (kind::f16, the default when the
-    point norms fit) and on fp32 features (kind::tf32, SAP_TC_F16=0) give the
-    same block product to fp32-level accuracy, and both match the oracle."""
+    point norms fit; 32 features for d <= 9, 64 with 128-byte rows above) and
+    on fp32 features (kind::tf32, SAP_TC_F16=0) give the same block product to
+    fp32-level accuracy, and both match the oracle."""
     rng = np.random.default_rng(11)
-    n, d, b, m = 20000, 9, 512, 65
+    n, b, m = 20000, 512, 65
     X = rng.standard_normal((n, d))
     ls = np.full(d, 3.0)
     W = rng.standard_normal((n, m))
