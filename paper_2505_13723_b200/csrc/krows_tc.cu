@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -415,6 +416,19 @@ size_t sap_krows_tc_workspace(int64_t b, int m, int64_t ncols) {
 
 // launch tags of the dynamic unit counter (any start value works)
 std::atomic<unsigned> g_tc_epoch{0x5a17u};
+// launch epochs per workspace, consecutive, so each launch finds the counter
+// slot the previous launch on that workspace armed for it (krows_tc2.cuh)
+std::mutex g_epoch_mu;
+std::unordered_map<const void *, unsigned> g_ws_epoch;
+unsigned next_epoch(const void *ws) {
+  std::lock_guard<std::mutex> lk(g_epoch_mu);
+  auto it = g_ws_epoch.find(ws);
+  if (it == g_ws_epoch.end()) {
+    if (g_ws_epoch.size() > 4096) g_ws_epoch.clear();  // bounded; a miss only costs one re-arm
+    it = g_ws_epoch.emplace(ws, g_tc_epoch.fetch_add(0x10000u, std::memory_order_relaxed)).first;
+  }
+  return ++it->second;
+}
 
 int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, int64_t bpad,
                       const int64_t *row_ids, int64_t b, int64_t col_base, const void *Zhi,
@@ -469,7 +483,7 @@ int sap_krows_tc_next(const void *CA, int64_t ncols, int ka, const void *RAg, in
     const char *st_env = getenv("SAP_TC_STATIC");
     if (ws_bytes >= part_bytes + 8 && !(st_env && atoi(st_env))) {
       p.sched = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + part_bytes);
-      p.epoch = g_tc_epoch.fetch_add(1u, std::memory_order_relaxed);
+      p.epoch = next_epoch(p.sched);
     }
   }
   // the next operand inside the CTA-pair kernel (16-byte vector rows only)

@@ -167,6 +167,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     tc::fence_barrier_init();
   }
+  if (p.sched && blockIdx.x == 0 && threadIdx.x == 0)  // arm the next launch's counter slot
+    p.sched[(p.epoch + 1u) & 1u] = static_cast<unsigned long long>(p.epoch + 1u) << 32;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tm_rows);
     tc::prefetch_tmap(&tm_cols);
@@ -219,17 +221,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (dyn && cr == 0) {  // the leader's producer fetches and publishes
           const int slot = k % kUR;
           tc::mbar_wait(tc::smem_u32(&u_empty[slot]), ((k / kUR) & 1) ^ 1);
-          // u = this launch's next unit: the counter is tagged with the launch's
-          // epoch, so no reset between launches is needed
-          unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(p.sched), prev;
-          do {
-            prev = old;
-            const bool mine = unsigned(old >> 32) == p.epoch;
-            const unsigned long long nxt =
-                (static_cast<unsigned long long>(p.epoch) << 32) | ((mine ? (old & 0xffffffffull) : 0ull) + 1ull);
-            u = mine ? int(old & 0xffffffffull) : 0;
-            old = atomicCAS(p.sched, prev, nxt);
-          } while (old != prev);
+          // u = this launch's next unit from its counter slot, tagged with the
+          // launch's epoch. The previous launch on this workspace armed the
+          // slot ((epoch << 32) | 0), so one atomicAdd is the whole fetch; a
+          // stale tag (first launch on a workspace) falls back to re-arming it
+          // by compare-and-swap. (A compare-and-swap loop for every fetch made
+          // 74 leaders retry against each other: ~10 us per unit at config 2.)
+          unsigned long long *slot_ctr = p.sched + (p.epoch & 1u);
+          unsigned long long old = atomicAdd(slot_ctr, 1ull), prev;
+          if (unsigned(old >> 32) == p.epoch) {
+            u = int(old & 0xffffffffull);
+          } else {
+            old = *reinterpret_cast<volatile unsigned long long *>(slot_ctr);
+            do {
+              prev = old;
+              const bool mine = unsigned(old >> 32) == p.epoch;
+              const unsigned long long nxt = (static_cast<unsigned long long>(p.epoch) << 32) |
+                                             ((mine ? (old & 0xffffffffull) : 0ull) + 1ull);
+              u = mine ? int(old & 0xffffffffull) : 0;
+              old = atomicCAS(slot_ctr, prev, nxt);
+            } while (old != prev);
+          }
           if (u >= units) u = -1;
           u_ring[slot] = u;
           tc::st_cluster_u32(tc::mapa(tc::smem_u32(&u_ring[slot]), 1), uint32_t(u));
