@@ -36,8 +36,8 @@ namespace pw {
 // clusters of 4 (128 CTAs) ran in 1.22 ms against 1.56 ms as 3.5 waves of
 // clusters of 16 -- and a small batch (the ramp's first, whose stepsize the
 // first step waits for) keeps 16 CTAs per iteration for latency.
-// SAP_POWER_CLUSTER forces one size.
-constexpr int kMaxCluster = 16;  // non-portable cluster size (B200 supports 16)
+// SAP_POWER_CLUSTER forces one size (16 is a non-portable cluster size,
+// which B200 supports).
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerPass = 4;  // rows a warp dots at once (amortises w reads)
