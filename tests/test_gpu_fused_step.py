@@ -99,8 +99,16 @@ def bounds(A, nz):
     return out
 
 
-def test_next_operand_and_fused_gradient_match_unfused_passes():
-    o, P, Q, Y, B, rng = _problem()
+@pytest.mark.parametrize("n,m,side", [(20000, 65, "1"), (20000, 65, None), (400000, 9, "1")])
+def test_next_operand_and_fused_gradient_match_unfused_passes(n, m, side, monkeypatch):
+    """side "1" forces the block-row kernel's side job (short columns per CTA:
+    the flat loop at n = 2e4; long ones: the column loop at n = 4e5); None
+    lets the launcher choose (here the separate pass)."""
+    if side is None:
+        monkeypatch.delenv("SAP_ZNEXT_SIDE", raising=False)
+    else:
+        monkeypatch.setenv("SAP_ZNEXT_SIDE", side)
+    o, P, Q, Y, B, rng = _problem(n=n, m=m)
     n, m, b = o.n, P.shape[0], B.size
     d = dev()
     tcp = o.tc_points()
