@@ -71,7 +71,9 @@ struct Args {
   int parts;      // partials T_k (stage 0's grid)
   int rows_per;    // block rows per CTA
   int do_grad, do_apply, has_next;
-  int stage;       // 0: A+B, 2: D (+E); C is phase4_reduce_kernel
+  int stage;       // 0: A (+B with tpart), 2: D (+E); C is phase4_ut_kernel or, with
+                   // tpart, phase4_reduce_kernel
+  int tpart;       // 1: B as per-CTA partials of stage 0 + C their sum (SAP_P4_TPART=1)
   int dbg;         // profiling: 5 skips B's product, 6 D's product, 7 the update,
                    // 8 the rebuild check (E), 9 the next operand's block rows
 };
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) phase4_kernel(const Args A) {
   const int64_t i0 = dmin(b, int64_t(blockIdx.x) * A.rows_per);
   const int64_t i1 = dmin(b, i0 + A.rows_per);
   const int ntl = m8 / 8;
-  const bool woodbury = A.do_apply && r > 0;
+  const bool woodbury = A.do_apply && r > 0 && (A.stage != 0 || A.tpart);
   // stream order with the previous stage (programmatic dependent launch: this
   // grid was scheduled early, its inputs are complete after the wait); the
   // next stage may then be scheduled, to wait in turn
@@ -410,6 +412,52 @@ __global__ void __launch_bounds__(kThreads, 2) phase4_reduce_kernel(const Args A
   if (q == 0 && o < rm) A.t[o] = s;
 }
 
+// ---------------- B + C in one: t = U^T g, one 8 x 8 tile of t per CTA ----------------
+// Every CTA reads all b rows of its 8 columns of U and of g (fp64, from L2)
+// and runs the K = b contraction on the FP64 tensor cores, the 16 warps each
+// taking every 16th group of four rows and their 8 x 8 partials summed in a
+// fixed order: no per-CTA r x m partials in HBM (with 148 CTAs of ~7-14 rows,
+// 7.7 MB written and read back per iteration at m = 65, r = 100) and no
+// separate summing launch.
+__global__ void __launch_bounds__(kThreads, 1) phase4_ut_kernel(const Args A) {
+  pdl_wait();
+  pdl_trigger();
+  const sap_step_args &a = A.a;
+  const int m = a.m, r = a.r;
+  const int ntl = (m + 7) / 8;
+  const int mt = blockIdx.x / ntl, nt = blockIdx.x % ntl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fg = lane >> 2, fq = lane & 3;
+  const int64_t b = a.b, steps = (b + 3) / 4;
+  const int ucol = mt * 8 + fg, gcol = nt * 8 + fg;
+  const bool uok = ucol < r, gok = gcol < m;
+  double d0 = 0.0, d1 = 0.0;
+  constexpr int kU = 4;  // k-steps whose loads are in flight together
+  for (int64_t k0 = warp; k0 < steps; k0 += int64_t(kWarps) * kU) {
+    double av[kU], bv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = (k0 + int64_t(u) * kWarps) * 4 + fq;
+      const bool ok = i < b;
+      av[u] = (ok && uok) ? __ldg(a.U + i * a.ldu + ucol) : 0.0;
+      bv[u] = (ok && gok) ? __ldcg(a.g + i * a.ldgo + gcol) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dmma(d0, d1, av[u], bv[u]);
+  }
+  __shared__ double red[kWarps][64];
+  red[warp][fg * 8 + 2 * fq] = d0;
+  red[warp][fg * 8 + 2 * fq + 1] = d1;
+  __syncthreads();
+  if (tid < 64) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += red[w][tid];
+    const int row = mt * 8 + tid / 8, col = nt * 8 + tid % 8;
+    if (row < r && col < m) A.t[int64_t(row) * m + col] = s;
+  }
+}
+
 }  // namespace p4
 }  // namespace sap
 
@@ -494,6 +542,10 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
     A.dbg = e ? atoi(e) : 0;
   }
   const bool woodbury = do_apply && a.r > 0;
+  {
+    const char *e = getenv("SAP_P4_TPART");
+    A.tpart = e && atoi(e) != 0;
+  }
   // stages, each one launch in stream order; programmatic dependent launch
   // lets the next stage's grid be scheduled while the previous one runs (it
   // waits in griddepcontrol.wait), so the launch gaps between them shrink
@@ -510,8 +562,9 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = getenv("SAP_P4_NO_PDL") ? 0 : 1;
-    const cudaError_t e = stage == 1 ? cudaLaunchKernelEx(&cfg, p4::phase4_reduce_kernel, A)
-                                     : cudaLaunchKernelEx(&cfg, p4::phase4_kernel, A);
+    const cudaError_t e = stage == 1   ? cudaLaunchKernelEx(&cfg, p4::phase4_reduce_kernel, A)
+                          : stage == 3 ? cudaLaunchKernelEx(&cfg, p4::phase4_ut_kernel, A)
+                                       : cudaLaunchKernelEx(&cfg, p4::phase4_kernel, A);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return fail(SAP_ERR_DEVICE, "block_step: stage %d launch failed: %s", stage,
@@ -520,10 +573,19 @@ int sap_block_step(const sap_step_args *args, int mode, void *ws, size_t ws_byte
     return check_launch("phase4_kernel");
   };
   int rc;
-  if ((do_grad || woodbury) && (rc = launch(0, G, smem)) != SAP_OK) return rc;
-  if (!do_apply) return SAP_OK;
-  if (woodbury && (rc = launch(1, int((rm * 16 + p4::kThreads - 1) / p4::kThreads), 0)) != SAP_OK)
-    return rc;
+  if (A.tpart) {  // stage 0 with per-CTA U^T g partials, summed by stage 1
+    if ((do_grad || woodbury) && (rc = launch(0, G, smem)) != SAP_OK) return rc;
+    if (!do_apply) return SAP_OK;
+    if (woodbury &&
+        (rc = launch(1, int((rm * 16 + p4::kThreads - 1) / p4::kThreads), 0)) != SAP_OK)
+      return rc;
+  } else {        // stage 0 (gradient rows only), then t = U^T g by 8 x 8 tiles
+    if (do_grad && (rc = launch(0, G, smem)) != SAP_OK) return rc;
+    if (!do_apply) return SAP_OK;
+    if (woodbury &&
+        (rc = launch(3, ((a.r + 7) / 8) * ((a.m + 7) / 8), 0)) != SAP_OK)
+      return rc;
+  }
   if ((rc = launch(2, G, smem)) != SAP_OK) return rc;
   return SAP_OK;
 }

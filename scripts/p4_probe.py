@@ -8,7 +8,9 @@ import paper_2505_13723_b200 as sap
 from paper_2505_13723_b200 import synthetic, _native as nat
 from paper_2505_13723_b200.solvers import AdasapEngine
 
-n, d, b, m, r = 1_000_000, 9, 2000, 65, 100
+# config 3 by default; N=100000 D=11 B=1000 FAM=rbf for config 2
+n, d, b = int(os.environ.get("N", "1000000")), int(os.environ.get("D", "9")), int(os.environ.get("B", "2000"))
+m, r = 65, 100
 prob = synthetic.make_problem(n, d, os.environ.get("FAM", "matern32"), m, seed=0, lam=1e-2,
                               device="cuda", rhs=os.environ.get("RHS", "noise"))
 o = sap.KernelOracle(prob.spec(), prob.X, prob.lam)
