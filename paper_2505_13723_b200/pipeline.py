@@ -152,6 +152,8 @@ class Lookahead:
 
     _WIDTH = int(os.environ.get("SAP_PRODUCE_WIDTH", "2"))  # batches produced concurrently
     _RAMP = max(2, int(os.environ.get("SAP_RAMP", "4")))    # batch-size growth of the ramp
+    # explicit leading batch sizes (SAP_RAMP_SIZES="1,4,8"), then growth by _RAMP
+    _SIZES = tuple(int(x) for x in os.environ.get("SAP_RAMP_SIZES", "").split(",") if x.strip())
 
     def __init__(self, oracle, shard, seed, b, r, lam, total, L, identity_precond, power_iters=10,
                  tcp=None, start=0):
@@ -277,9 +279,11 @@ class Lookahead:
     def _has_batch(self, k):
         """Define batches up to k (lazily); False past the iteration budget."""
         while len(self.bounds) <= k + 1 and (self.total is None or self.bounds[-1] < self.total):
-            nxt = self.bounds[-1] + self._c
+            j = len(self.bounds) - 1  # index of the batch being defined
+            c = min(self._SIZES[j], self.L) if j < len(self._SIZES) else self._c
+            nxt = self.bounds[-1] + c
             self.bounds.append(nxt if self.total is None else min(self.total, nxt))
-            self._c = min(self._RAMP * self._c, self.L)
+            self._c = min(self._RAMP * c, self.L)
         return len(self.bounds) > k + 1
 
     def _submit(self, k):

@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2505_13723_b200 import kernels as K
-L, b, r = int(os.environ.get("PL", "8")), 2000, 100
+L, b, r = int(os.environ.get("PL", "8")), int(os.environ.get("B", "2000")), 100
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(0)
 A = torch.randn(L, b, b, device=dev, generator=g) / b
