@@ -371,7 +371,7 @@ def _as2d(A):
 
 _STAGE = {"buf": None}
 _STAGE_CHUNK = int(os.environ.get("SAP_READBACK_CHUNK", str(1 << 23)))  # elements per chunk
-_WIDEN_TASKS = int(os.environ.get("SAP_READBACK_TASKS", "8"))
+_WIDEN_TASKS = int(os.environ.get("SAP_READBACK_TASKS", "0")) or xfer._TASKS
 
 
 def _staging(elems):

@@ -36,7 +36,21 @@ def mark(tag):
 
 _UP = {"buf": None}
 _UP_CHUNK = 1 << 23  # elements per chunk
-_TASKS = 8           # host conversion tasks per chunk
+def _host_threads():
+    try:
+        cores = len(_os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        cores = _os.cpu_count() or 8
+    return max(2, min(8, cores))
+
+
+# host conversion tasks per chunk (and the pool's threads): the casting copies
+# are memory-bound, and a fresh float64 output's first touch (the kernel
+# zeroing its pages) scales with threads: 55 ms on one thread for 520 MB, 11
+# ms on eight (scripts/readback_probe.py). Twelve threads read W back ~2 ms
+# faster on a 16-core box but slowed the concurrent steps as much (e2e
+# 88.0-88.8 ms either way), so eight; SAP_HOST_THREADS overrides
+_TASKS = int(_os.environ.get("SAP_HOST_THREADS", "0")) or _host_threads()
 _POOL = {"ex": None}
 _POOL_LOCK = threading.Lock()
 
