@@ -111,6 +111,15 @@ def test_contract_errors():
             sap.col_dist_matmul(o, np.zeros((20, 1)), bad)
     with pytest.raises(sap.ContractError):
         sap.col_dist_matmul(o, np.zeros((19, 1)), np.array([1]))
+    # non-finite training inputs (kernels.py:100-112), host array and CUDA tensor
+    for bad in (np.inf, np.nan):
+        X = np.zeros((20, 2))
+        X[7, 1] = bad
+        with pytest.raises(sap.ValidationError):
+            sap.KernelOracle(sap.KernelSpec("rbf", np.ones(2)), X, 0.5)
+        with pytest.raises(sap.ValidationError):
+            sap.KernelOracle(sap.KernelSpec("rbf", np.ones(2)), torch.as_tensor(X, device="cuda"),
+                             0.5)
 
 
 def test_nystrom_and_woodbury_match_reference():
