@@ -127,8 +127,13 @@ __device__ __forceinline__ void split_range(int64_t tiles, int splits, int s, in
 // P = 2^14 k from the GEMM1 output S: for RBF S = 14 - s already (the offset
 // and sign ride in the augmented features, build_aug_kernel); a tiny positive
 // excess from rounding near s = 0 is harmless. Matern: S = s.
+// Matern distance t = sqrt(|s|) (one MUFU.SQRT, the |.| folded into its
+// operand) by default; SAP_MATERN_RSQ=1: t = s * rsqrt(max(s, 1e-30)) (two
+// more instructions). Round 1 measured the sqrt form 0.9% slower; with the
+// out-of-phase epilogue and the one-atomicAdd unit fetch it is 5.5% faster
+// (config 3 krows 1.345-1.350 -> 1.270-1.275 ms, 3 A/B pairs)
 #ifndef SAP_MATERN_RSQ
-#define SAP_MATERN_RSQ 1
+#define SAP_MATERN_RSQ 0
 #endif
 template <int FAM, bool POLY = false>
 __device__ __forceinline__ float pvalue(float s) {
@@ -144,10 +149,8 @@ __device__ __forceinline__ float pvalue(float s) {
     return kPScale * c;
   } else {
     // the 2^14 scale rides on the polynomial, so ex2 takes -t directly;
-    // t = s * rsqrt(s) with s floored at 1e-30 (which also clamps negative
-    // rounding, so s <= 0 gives t ~ 0). The alternative t = sqrt(|s|) (one
-    // MUFU.SQRT, |.| folded, two instructions fewer) measured 0.9% slower at
-    // config 3: the epilogue is bound by the MUFU pipe and its latency, not issue
+    // t = sqrt(|s|): |.| absorbs negative rounding near s = 0 (t ~ 0, k ~ 1)
+    // and s = 0 gives t = 0 exactly (the rsqrt form needs a floor there)
 #if SAP_MATERN_RSQ
     s = fmaxf(s, 1e-30f);
     const float t = s * rsqrt_approx(s);
