@@ -136,6 +136,14 @@ int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, i
 int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64_t strideSq,
                         int b, int count, int ldx, int d, int family, double variance, float *out,
                         int64_t ldo, int64_t strideOut, void *stream);
+/* The same, and K / variance split into fp16 hi + lo ([count] x [b][ldh]
+ * each, outh/outl + q*strideH): the operands of the lookahead's three-pass
+ * tensor-core sketch K_BB Omega (replaces the fp32 row_dist_matmul of
+ * dist.py:130-147). outh = NULL: sap_ktile_f32_batch. */
+int sap_ktile_f32_batch_split(const float *X, int64_t strideX, const float *xsq,
+                              int64_t strideSq, int b, int count, int ldx, int d, int family,
+                              double variance, float *out, int64_t ldo, int64_t strideOut,
+                              void *outh, void *outl, int64_t ldh, int64_t strideH, void *stream);
 
 /*
  * Batched preconditioned power-iteration stepsize (replaces randnla.py:165-196

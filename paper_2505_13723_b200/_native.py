@@ -47,6 +47,8 @@ SIGNATURES = {
     "sap_ktile64": (_I, [_P, _P, _I, _P, _I64, _P, _I64, _I, _D, _P, _I64, _P]),
     "sap_ktile_f32": (_I, [_P, _P, _P, _I64, _P, _P, _P, _I64, _I, _I, _I, _D, _P, _I64, _P]),
     "sap_ktile_f32_batch": (_I, [_P, _I64, _P, _I64, _I, _I, _I, _I, _I, _D, _P, _I64, _I64, _P]),
+    "sap_ktile_f32_batch_split": (_I, [_P, _I64, _P, _I64, _I, _I, _I, _I, _I, _D, _P, _I64, _I64,
+                                       _P, _P, _I64, _I64, _P]),
     "sap_power_stepsize": (_I, [_P, _I64, _I64, _P, _I64, _I, _P, _P, _P, _I, _I, _D, _I, _P,
                                 _P, _P]),
     "sap_grad_gather": (_I, [_P, _I64, _P, _P, _P, _I64, _D, _D, _P, _I64, _I, _D, _P, _I64, _P]),

@@ -5,6 +5,7 @@
 #include <string>
 #include <algorithm>
 #include <atomic>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "krows_ffma.cuh"
@@ -121,11 +122,15 @@ __global__ void __launch_bounds__(256)
 // ktile_kernel's (same fma order, same sum of norms, the id rule on the
 // diagonal: the block's ids are unique, so i == j), so the values are the
 // same bit for bit; ~5x faster than the 32x32 tiles at b = 2000.
+// Optionally (outh != NULL) also K / variance split into fp16 hi + lo (the
+// sketch's three-pass tensor-core GEMM operand, pipeline.py): hi = fp16(k),
+// lo = fp16(k - hi), k = K / variance in [0, 1].
 template <int FAM>
 __global__ void __launch_bounds__(256)
     ktile_batch_kernel(const float *X, int64_t strideX, const float *xsq, int64_t strideSq, int b,
                        int ldx, int d, float variance, float *out, int64_t ldo,
-                       int64_t strideOut) {
+                       int64_t strideOut, __half *outh, __half *outl, int64_t ldh,
+                       int64_t strideH) {
   extern __shared__ __align__(16) float sh[];
   float *sA = sh;            // [d][64] row points
   float *sC = sh + d * 64;   // [d][64] column points
@@ -176,6 +181,23 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if (j + c < b) o[c] = v[c];
+    }
+    if (outh) {
+      const float iv = 1.0f / variance;
+      __half hh[4], ll[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float k = v[c] * iv;
+        hh[c] = __float2half_rn(k);
+        ll[c] = __float2half_rn(k - __half2float(hh[c]));
+      }
+      const int64_t ho = int64_t(q) * strideH + int64_t(i) * ldh + j;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (j + c < b) {
+          outh[ho + c] = hh[c];
+          outl[ho + c] = ll[c];
+        }
     }
   }
 }
@@ -561,13 +583,17 @@ int sap_ktile_f32(const float *Ra, const float *rasqn, const int64_t *row_ids, i
                       out, ldo, stream);
 }
 
-int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64_t strideSq,
-                        int b, int count, int ldx, int d, int family, double variance, float *out,
-                        int64_t ldo, int64_t strideOut, void *stream) {
+int sap_ktile_f32_batch_split(const float *X, int64_t strideX, const float *xsq,
+                              int64_t strideSq, int b, int count, int ldx, int d, int family,
+                              double variance, float *out, int64_t ldo, int64_t strideOut,
+                              void *outh, void *outl, int64_t ldh, int64_t strideH,
+                              void *stream) {
   if (b <= 0 || count <= 0 || ldx < d || d < 1 || d > 64 || ldo < b || ldo % 4 ||
-      strideOut % 4 || (reinterpret_cast<uintptr_t>(out) & 15))
+      strideOut % 4 || (reinterpret_cast<uintptr_t>(out) & 15) || (outh && (!outl || ldh < b)) ||
+      !(variance > 0.0))
     return fail(SAP_ERR_CONTRACT, "ktile_f32_batch: bad shape b=%d d=%d ldo=%lld", b, d,
                 (long long)ldo);
+  __half *oh = static_cast<__half *>(outh), *ol = static_cast<__half *>(outl);
   dim3 grid(unsigned((b + 63) / 64), unsigned((b + 63) / 64), unsigned(count));
   const size_t smem = size_t(2 * 64 * d) * sizeof(float);
   cudaStream_t st = S(stream);
@@ -575,19 +601,29 @@ int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64
   switch (family) {
     case SAP_RBF:
       ktile_batch_kernel<SAP_RBF><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b, ldx, d,
-                                                           var, out, ldo, strideOut);
+                                                           var, out, ldo, strideOut, oh, ol, ldh,
+                                                           strideH);
       break;
     case SAP_MATERN32:
       ktile_batch_kernel<SAP_MATERN32><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b,
-                                                                ldx, d, var, out, ldo, strideOut);
+                                                                ldx, d, var, out, ldo, strideOut,
+                                                                oh, ol, ldh, strideH);
       break;
     case SAP_MATERN52:
       ktile_batch_kernel<SAP_MATERN52><<<grid, 256, smem, st>>>(X, strideX, xsq, strideSq, b,
-                                                                ldx, d, var, out, ldo, strideOut);
+                                                                ldx, d, var, out, ldo, strideOut,
+                                                                oh, ol, ldh, strideH);
       break;
     default: return fail(SAP_ERR_CONTRACT, "ktile_f32_batch: unknown family %d", family);
   }
   return check_launch("ktile_batch_kernel");
+}
+
+int sap_ktile_f32_batch(const float *X, int64_t strideX, const float *xsq, int64_t strideSq,
+                        int b, int count, int ldx, int d, int family, double variance, float *out,
+                        int64_t ldo, int64_t strideOut, void *stream) {
+  return sap_ktile_f32_batch_split(X, strideX, xsq, strideSq, b, count, ldx, d, family, variance,
+                                   out, ldo, strideOut, nullptr, nullptr, 0, 0, stream);
 }
 
 int sap_grad_gather(const float *G, int64_t ldg, const float *P, const float *Q, const float *Y,

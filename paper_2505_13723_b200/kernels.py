@@ -327,6 +327,16 @@ def ktile_f32_batch(spec, X, xsq, d, out):
     return out
 
 
+def ktile_f32_batch_split(spec, X, xsq, d, out, outh, outl):
+    """ktile_f32_batch, plus K / variance as fp16 hi + lo into outh / outl
+    ((count, b, ldh) each): the three-pass tensor-core sketch's operands."""
+    count, b, ldx = X.shape
+    nat.call("sap_ktile_f32_batch_split", nat.ptr(X), X.stride(0), nat.ptr(xsq), xsq.stride(0), b,
+             count, ldx, d, spec.code, spec.variance, nat.ptr(out), out.stride(1), out.stride(0),
+             nat.ptr(outh), nat.ptr(outl), outh.stride(1), outh.stride(0), nat.stream_handle())
+    return out
+
+
 def power_stepsize(Kbb, U, E, rho, v0, lam, iters, eta, bad):
     """Batched preconditioned power iteration (randnla.py:165-196) over the
     leading ``Kbb.shape[0]`` problems: eta[q] = 1/(v.Hv), bad[q] |= failure."""

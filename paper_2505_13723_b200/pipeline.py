@@ -221,7 +221,20 @@ class Lookahead:
         # the sketch K[B,B] Omega: by default a batched fp32 GEMM against the
         # K_BB tiles the power iteration needs anyway (SAP_SKETCH=tc: the
         # block-row kernel with the block's own points as columns, round 1)
-        self.sketch_gemm = os.environ.get("SAP_SKETCH", "gemm") == "gemm"
+        mode = os.environ.get("SAP_SKETCH", "gemm")
+        self.sketch_gemm = mode in ("gemm", "gemm32")
+        # the GEMM in three fp16 tensor-core passes (K_BB / variance and Omega
+        # split hi + lo by the tile kernel / here, fp32 accumulation: 0.25 ms
+        # against 0.63 ms for the fp32 SIMT GEMM per batch of 31 at b = 2000,
+        # 3.2e-6 against 2.2e-6 relative error; scripts/sketch_probe.py); the
+        # fp16 copies cost 2 b^2 bytes per slot iteration, so only up to
+        # b = 4096 (SAP_SKETCH=gemm32: the fp32 GEMM)
+        self.sketch_split = mode == "gemm" and bool(self.r) and b <= 4096
+        if self.sketch_split:
+            ldh = (b + 7) // 8 * 8
+            for slot in self.slots:
+                slot.Kh = torch.empty((self.L, b, ldh), dtype=torch.float16, device=dev)
+                slot.Kl = torch.empty((self.L, b, ldh), dtype=torch.float16, device=dev)
         self.tc_sketch = (not self.sketch_gemm and tcp is not None and self.r and b >= 512
                           and oracle.use_tc(self.r))
         if self.tc_sketch:
@@ -476,7 +489,22 @@ class Lookahead:
             if self.tcp is not None:
                 self.tcp.gather_rows_batch(bd, slot.RAg[:count])
                 xfer.mark("gather rows")
-            if r and self.sketch_gemm:
+            if r and self.sketch_split:
+                # K_BB once per iteration (the power iteration's operand), and
+                # K_BB / variance as fp16 hi + lo; the sketch K_BB Omega
+                # (row_dist_matmul, dist.py:130-147) = variance (Kh Oh + Kh Ol +
+                # Kl Oh) in two batched tensor-core GEMMs, fp32 accumulation
+                K.ktile_f32_batch_split(self.o.spec, slot.Xb[:count], slot.rsq[:count], pts.d,
+                                        slot.Kbb[:count], slot.Kh[:count], slot.Kl[:count])
+                xfer.mark("kbb")
+                oh = om.to(torch.float16)
+                ohl = torch.cat([oh, (om - oh.to(torch.float64)).to(torch.float16)], dim=2)
+                o1 = torch.bmm(slot.Kh[:count, :, :b], ohl, out_dtype=torch.float32)
+                o2 = torch.bmm(slot.Kl[:count, :, :b], oh, out_dtype=torch.float32)
+                torch.add(o1[:, :, :r], o1[:, :, r:], out=sketch)
+                sketch.add_(o2).mul_(self.o.spec.variance)
+                xfer.mark("sketch")
+            elif r and self.sketch_gemm:
                 # K_BB once per iteration (the power iteration's operand too),
                 # then the sketch K_BB Omega as one batched fp32 GEMM
                 # (row_dist_matmul, dist.py:130-147; 2 b^2 r flop per iteration)
