@@ -5,9 +5,10 @@
 //
 //   A  g[i, c]  = sum_s part[s][c][i] * variance / (2^14 zscale_c)      (K[B,:] Z)
 //               + lam * Z[B_i, c] - Y[B_i, c]                 solvers.py:376-377
-//   B  T_k      = U[rows_k]^T g[rows_k]             (per-CTA partial, r x m)
 //   -- launch --
-//   C  t        = sum_k T_k                          (fixed order)
+//   B+C t       = U^T g, one 8 x 8 tile per CTA over all b rows (phase4_ut_kernel)
+//               (SAP_P4_TPART=1: B as per-CTA partials T_k = U[rows_k]^T g[rows_k]
+//               in stage A, C their fixed-order sum, phase4_reduce_kernel)
 //   -- launch --
 //   D  D[i, :]  = g[i, :] - (U Mc)[i, :] t          randnla.py:109-134 (1/rho rides
 //                                                   on the stepsize eta/rho)
@@ -16,7 +17,7 @@
 //   E  if an updated block row left the next operand's scale: the last CTA of
 //      D rebuilds it (rare: the scale leaves 64x headroom)
 //
-// The two small fp64 GEMMs (B: r x m x rows, D: rows x m x r per CTA) run on
+// The two small fp64 GEMMs (B: r x m x b, D: rows x m x r per CTA) run on
 // the FP64 tensor cores (mma.sync m8n8k4 .f64) from shared-memory tiles laid
 // out so every fragment load is bank-conflict free. Every reduction runs in a
 // fixed order (no floating-point atomics): the result is bitwise
