@@ -332,3 +332,27 @@ def test_long_trajectory_full_lookahead_batches():
     etas = np.array([rec.stepsize for rec in res.trace.records])
     assert np.abs(etas - eta_ref).max() / np.abs(eta_ref).max() < 1e-4
     assert rel(res.W, W_ref) < 2e-3
+
+
+def test_vector_inputs_return_vectors():
+    """1-D right-hand sides and operands come back 1-D (reference dist.py:113-127,
+    :135-147; solvers.py:243-247, :451), equal to the (n, 1) results."""
+    rng = np.random.default_rng(17)
+    n, d, b = 3000, 5, 256
+    X = rng.standard_normal((n, d))
+    o = sap.KernelOracle(sap.KernelSpec("matern32", np.full(d, 2.0), 1.0), X, 1e-1)
+    w = rng.standard_normal(n)
+    B = np.sort(rng.choice(n, b, replace=False))
+    g1 = sap.col_dist_matmul(o, w, B)
+    g2 = sap.col_dist_matmul(o, w[:, None], B)
+    assert g1.shape == (b,) and np.array_equal(g1, g2[:, 0])
+    om = rng.standard_normal(b)
+    s1 = sap.row_dist_matmul(o, om, B)
+    assert s1.shape == (b,)
+    cfg = sap.RunConfig(lam=1e-1, blocksize=b, nystrom_rank=32, max_iters=20, residual_every=0,
+                        seed=3)
+    y = rng.standard_normal(n)
+    r1 = sap.adasap_solve(o, y, cfg)
+    r2 = sap.adasap_solve(o, y[:, None], cfg)
+    assert r1.W.shape == (n,) and r2.W.shape == (n, 1)
+    assert np.abs(r1.W - r2.W[:, 0]).max() <= 1e-6 * np.abs(r2.W).max()
