@@ -9,9 +9,10 @@
 // iteration of a lookahead batch). CTA c of the cluster owns rows [lo, hi) of
 // K_BB (fp32, the values the tile kernel computes) and of U (fp64); the
 // length-b vector w = P^{-1/2} v is replicated in every CTA's shared memory
-// by DSMEM broadcast, and the three reductions of a step (U^T v, U^T z and
-// the two scalars v.y, |y|^2) combine per-CTA partials read over DSMEM in a
-// fixed rank order, so every CTA holds bitwise-identical results. K_BB is
+// by DSMEM broadcast, and the two reductions of a step (U^T z and the two
+// scalars v.y = w.z, |y|^2 = z.P^{-1} z) combine per-CTA partials read over
+// DSMEM in a fixed rank order, so every CTA holds bitwise-identical results
+// (the loop runs on w, see the kernel; the iterates are the reference's). K_BB is
 // streamed once per step (b^2 * 4 bytes): the kernel is bound by L2/HBM
 // bandwidth, replacing ~12 batched cuBLAS/elementwise launches per step.
 #include <cooperative_groups.h>
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   __syncthreads();
 
   // coef = E * (U^T x) over the cluster, x given on own rows
-  auto ut_times = [&](const double *x) {
+  // (or F * (U^T x), F = 1/(S+rho) - 1/rho = E (E + 2/sqrt(rho)), with pinv)
+  auto ut_times = [&](const double *x, bool pinv) {
     if (r <= kThreads) {
       // kThreads / r row groups per column, combined in a fixed order
       const int G = kThreads / r, g = tid / r, k = tid % r;
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
       double s = 0.0;
 #pragma unroll
       for (int c = 0; c < kCluster; ++c) s += v[c];
-      coef[k] = E[k] * s;
+      coef[k] = (pinv ? E[k] * fma(2.0, isr, E[k]) : E[k]) * s;
     }
     __syncthreads();
   };
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   auto apply_u = [&](const double *x, double *out) {
     for (int i0 = 0; i0 < nloc; i0 += kThreads / kSplit) {
       const int i = i0 + tid / kSplit;
-      const double s = row_dot(i);
+      const double s = r ? row_dot(i) : 0.0;
       if (part_id == 0 && i < nloc) out[i] = fma(x[i], isr, s);
     }
     __syncthreads();
@@ -194,18 +196,28 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
 #else
 #define PP(k) do {} while (0)
 #endif
-  for (int it = 0; it < a.iters; ++it) {
-    // w = P^{-1/2} v on own rows -> broadcast (fp32) into every CTA's wf
-    if (r) ut_times(vloc);
-    PP(0);
-    apply_u(vloc, zloc);  // zloc holds w (own rows) for the moment
-    PP(1);
+  // The iteration runs on w = P^{-1/2} v rather than on v (the same iterates,
+  // Rayleigh quotients and norms, reassociated):
+  //   z = (K + lam I) w,  est = v.y = w.z,  |y|^2 = z.P^{-1} z = z.u,
+  //   u = P^{-1} z = z/rho + U diag(F) U^T z,  w <- u/|y|,
+  // two passes over the CTA's U rows per step instead of four (U^T v, U coef,
+  // U^T z, U coef) and one cluster barrier fewer; w_0 = P^{-1/2} v_0 once.
+  const double irho = 1.0 / rho;
+  auto broadcast_w = [&]() {  // own rows of w (vloc) -> every CTA's wf, fp32
     for (int c = 0; c < kCluster; ++c) {
       float *dst = cluster.map_shared_rank(wf, c);
-      for (int i = tid; i < nloc; i += kThreads) dst[lo + i] = float(zloc[i]);
+      for (int i = tid; i < nloc; i += kThreads) dst[lo + i] = float(vloc[i]);
     }
     cluster.sync();
-    PP(2);
+  };
+  if (r) ut_times(vloc, false);
+  apply_u(vloc, zloc);
+  for (int i = tid; i < nloc; i += kThreads) vloc[i] = zloc[i];
+  __syncthreads();
+  broadcast_w();
+  PP(0);
+  // vloc and zloc hold w on own rows at the top of a step
+  for (int it = 0; it < a.iters; ++it) {
     // z = K w + lam w on own rows: a warp dots kRowsPerPass rows at once, fp32
     // products summed per lane (64 terms for b = 2000), lanes combined in fp64
     for (int i0 = warp * kRowsPerPass; i0 < nloc; i0 += kWarps * kRowsPerPass) {
@@ -264,18 +276,19 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
     }
     __syncthreads();
     PP(3);
-    // y = P^{-1/2} z on own rows
-    if (r) ut_times(zloc);
+    // u = P^{-1} z on own rows, the partials of w.z and z.u
+    if (r) ut_times(zloc, true);
     PP(4);
     double dvy = 0.0, dyy = 0.0;
     for (int i0 = 0; i0 < nloc; i0 += kThreads / kSplit) {
       const int i = i0 + tid / kSplit;
       const double s = r ? row_dot(i) : 0.0;
       if (part_id == 0 && i < nloc) {
-        const double y = fma(zloc[i], isr, s);
-        dvy = fma(vloc[i], y, dvy);
-        dyy = fma(y, y, dyy);
-        zloc[i] = y;
+        const double z = zloc[i];
+        const double u = fma(z, irho, s);
+        dvy = fma(vloc[i], z, dvy);
+        dyy = fma(z, u, dyy);
+        zloc[i] = u;
       }
     }
     PP(5);
@@ -299,19 +312,26 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
       yy += sv[2 * c + 1];
     }
     est = vy;
-    const double ny = sqrt(yy);
-    bad = bad || ny == 0.0;
-    const double inv = ny > 0.0 ? 1.0 / ny : 0.0;
-    for (int i = tid; i < nloc; i += kThreads) vloc[i] = zloc[i] * inv;
-    PP(6);
-    // peers read this CTA's part/spart/wf only before the next cluster.sync
-    // of the following step, which every CTA reaches after these reads
+    bad = bad || !(yy > 0.0);  // |y| = 0 (z = 0); a rounding-negative z.P^{-1}z alike
+    const double inv = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
+    for (int i = tid; i < nloc; i += kThreads) {
+      const double w = zloc[i] * inv;
+      vloc[i] = w;
+      zloc[i] = w;
+    }
     __syncthreads();
+    PP(6);
+    // every CTA has finished this step's sweep (reading its wf) and its reads
+    // of the peers' part before the scalar barrier above, and reads the
+    // peers' spart before the broadcast's barrier: no peer data is overwritten
+    // while still needed
+    if (it + 1 < a.iters) broadcast_w();
+    PP(2);
   }
 #ifdef SAP_POWER_PROF
   if (blockIdx.x == 0 && tid == 0)
-    printf("power prof (cycles): ut_v %llu apply_w %llu bcast+sync %llu gemv %llu ut_z %llu y %llu "
-           "red+sync %llu\n", tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp[6]);
+    printf("power prof (cycles): w0 %llu bcast+sync %llu gemv %llu ut_z %llu u %llu "
+           "red+sync %llu\n", tp[0], tp[2], tp[3], tp[4], tp[5], tp[6]);
 #endif
   bad = bad || !(est > 0.0);
   if (crank == 0 && tid == 0) {
