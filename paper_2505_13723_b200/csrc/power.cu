@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   double *coef = part + r;            // [r]     E * (U^T x), full
   double *spart = coef + r;           // [2]     own partial of v.y, |y|^2
   double *red = spart + 2;            // [2*kWarps] block reduction scratch
-  double *scratch = red + 2 * kWarps; // [kThreads]
-  float *wf = reinterpret_cast<float *>(scratch + kThreads);  // [b4] replicated w (fp32)
+  double *scratch = red + 2 * kWarps; // [2*kThreads]
+  float *wf = reinterpret_cast<float *>(scratch + 2 * kThreads);  // [b4] replicated w (fp32)
   double *us = reinterpret_cast<double *>(wf + b4);           // [nloc][r] own U rows (opt.)
 
   const float *K = a.K + int64_t(q) * a.strideK;
@@ -125,8 +125,43 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
 
   // coef = E * (U^T x) over the cluster, x given on own rows
   // (or F * (U^T x), F = 1/(S+rho) - 1/rho = E (E + 2/sqrt(rho)), with pinv)
+  const bool u_vec2 = (r & 1) == 0 && r / 2 <= kThreads &&
+                      (reinterpret_cast<uintptr_t>(U) & 15) == 0;
   auto ut_times = [&](const double *x, bool pinv) {
-    if (r <= kThreads) {
+    if (u_vec2) {
+      // column pairs (16-byte loads), kThreads / (r/2) row groups, two rows per
+      // trip with their own running sums: four independent fp64 chains and
+      // eight loads in flight per thread (the one-column form was latency-bound
+      // on L2 at ~23 B/clk per SM); groups combined in a fixed order
+      const int r2 = r >> 1, G = kThreads / r2, g = tid / r2, k2 = tid % r2;
+      double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+      if (g < G) {
+        const double2 *U2 = reinterpret_cast<const double2 *>(U);
+        int i = g;
+#pragma unroll 4
+        for (; i + G < nloc; i += 2 * G) {
+          const double2 ua = U2[i * r2 + k2], uc = U2[(i + G) * r2 + k2];
+          const double xa = x[i], xc = x[i + G];
+          s0 = fma(ua.x, xa, s0);
+          s1 = fma(ua.y, xa, s1);
+          t0 = fma(uc.x, xc, t0);
+          t1 = fma(uc.y, xc, t1);
+        }
+        if (i < nloc) {
+          const double2 ua = U2[i * r2 + k2];
+          s0 = fma(ua.x, x[i], s0);
+          s1 = fma(ua.y, x[i], s1);
+        }
+      }
+      scratch[2 * tid] = s0 + t0;
+      scratch[2 * tid + 1] = s1 + t1;
+      __syncthreads();
+      if (tid < r) {
+        double t = 0.0;
+        for (int gg = 0; gg < G; ++gg) t += scratch[2 * (gg * r2 + (tid >> 1)) + (tid & 1)];
+        part[tid] = t;
+      }
+    } else if (r <= kThreads) {
       // kThreads / r row groups per column, combined in a fixed order
       const int G = kThreads / r, g = tid / r, k = tid % r;
       double s = 0.0;
@@ -170,7 +205,20 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   const int kq = (r + kSplit - 1) / kSplit, part_id = tid % kSplit;
   auto row_dot = [&](int i) {
     double s = 0.0;
-    if (i < nloc) {
+    if (i < nloc && u_vec2) {
+      // the kSplit lanes of a row take interleaved column pairs: 64
+      // contiguous bytes per row and load, two running sums per lane
+      const double2 *u2 = reinterpret_cast<const double2 *>(U + i * r);
+      const double2 *c2 = reinterpret_cast<const double2 *>(coef);
+      double sa = 0.0, sb = 0.0;
+#pragma unroll 4
+      for (int k2 = part_id; k2 < (r >> 1); k2 += kSplit) {
+        const double2 u = u2[k2], c = c2[k2];
+        sa = fma(u.x, c.x, sa);
+        sb = fma(u.y, c.y, sb);
+      }
+      s = sa + sb;
+    } else if (i < nloc) {
       const double *ur = U + i * r;
       const int k1 = min(r, (part_id + 1) * kq);
       for (int k = part_id * kq; k < k1; ++k) s = fma(ur[k], coef[k], s);
@@ -368,7 +416,7 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
     return fail(SAP_ERR_CONTRACT, "power_stepsize: cluster size %d (4, 8 or 16)", C);
   const int per = (b + C - 1) / C;
   const size_t base = sizeof(double) * (2 * size_t(per) + 2 * size_t(r) + 2 + 2 * pw::kWarps +
-                                        pw::kThreads) +
+                                        2 * pw::kThreads) +
                       sizeof(float) * size_t((b + 3) & ~3);
   const size_t with_u = base + sizeof(double) * size_t(per) * size_t(r);
   constexpr size_t kCap = 200 * 1024;
