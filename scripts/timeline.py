@@ -60,3 +60,17 @@ for e in ev:
 print("per-iteration kernel time by stream (us/iter, launches/iter):")
 for (sid, name), (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:int(os.environ.get("TOPK", "40"))]:
     print(f"  s{sid} {t/NIT:8.1f} us  {c/NIT:5.2f}x  {name}")
+# what separates consecutive block-row products: the interval from one krows
+# kernel's end to the next one's start, and every kernel (any stream) that
+# starts inside it, for a few sample intervals
+krs = [e for e in ev if "krows_tc2_kernel<" in e["name"] and ", 80," in e["name"]]
+ivs = [(a["ts"] + a["dur"], b["ts"]) for a, b in zip(krs, krs[1:])]
+if ivs:
+    w = sorted(f - s for s, f in ivs)
+    print(f"krows->krows interval: median {w[len(w)//2]:.1f} us, mean {sum(w)/len(w):.1f} us, "
+          f"max {w[-1]:.1f} us over {len(w)}")
+    for s, f in ivs[:int(os.environ.get("SHOWIV", "4"))]:
+        print(f"  interval {f - s:.1f} us:")
+        for e in ev:
+            if s - 1 <= e["ts"] < f:
+                print(f"    +{e['ts'] - s:7.1f} {e['dur']:7.1f} us s{e['args'].get('stream')} {e['name'][:60]}")
