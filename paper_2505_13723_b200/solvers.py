@@ -304,7 +304,7 @@ class SolverState:
         cur = getattr(self, "_" + which)
         e = self._e
         if cur is None and e is not None:
-            cur = _to_host64(e.gather_full(e.materialize(which)))
+            cur = _to_host64(e.gather_full(e.materialize(which)), out=e.take_readback())
             if e.vector:
                 cur = cur[:, 0]
             setattr(self, "_" + which, cur)
@@ -384,15 +384,17 @@ def _staging(elems):
     return buf
 
 
-def _to_host64(t):
-    """Device tensor -> fresh C-contiguous float64 numpy array.
+def _to_host64(t, out=None):
+    """Device tensor -> fresh C-contiguous float64 numpy array (``out``: a
+    pre-faulted array of the same shape to fill instead, xfer.prefaulted).
 
     fp32 state is copied as fp32 (half the bytes of a widened copy) through a
     pinned double buffer: the device->host copy of chunk k overlaps the host
     threads widening chunk k-1 into the output (numpy's casting copy releases
     the GIL), which also spreads the output's first-touch page faults."""
     src = t.contiguous()
-    out = np.empty(tuple(src.shape), dtype=np.float64)
+    if out is None or out.shape != tuple(src.shape) or not out.flags.c_contiguous:
+        out = np.empty(tuple(src.shape), dtype=np.float64)
     flat_out = out.reshape(-1)
     if src.dtype != torch.float32 or src.device.type != "cuda" or src.numel() < (1 << 20):
         torch.from_numpy(out).copy_(src.to(torch.float64))
@@ -562,9 +564,25 @@ class AdasapEngine:
     def close(self):
         self.la.close()
 
+    def prepare_readback(self):
+        """Have host threads fault in the float64 array of the next full-iterate
+        readback (n x m) while the device works (xfer.prefaulted); the first
+        W/V/Z readback takes it."""
+        self._readback = xfer.prefaulted((self.n, self.m)) if self.n * self.m >= (1 << 20) else None
+
+    def take_readback(self):
+        rb, self._readback = getattr(self, "_readback", None), None
+        if rb is None:
+            return None
+        out, futs = rb
+        for f in futs:
+            f.result()
+        return out
+
     def release(self):
         """close() and drop the device buffers (state, operands, workspaces)
         so the caching allocator can hand them to the next engine at once."""
+        self._readback = None
         self.close()
         for name in ("P", "Q", "Y", "G", "g", "WB", "etas", "zop", "zop_next", "ws", "p4ws",
                      "Pb", "Qb", "W0", "tcp"):
@@ -907,6 +925,7 @@ def adasap_step(oracle, state, Y, config, accel, pool=None, identity_precond=Fal
                          state=None if zero else (state._W, state._V, state._Z))
         e.bind_key = key
         e.Y_src = Y  # keeps id(Y) valid while bound
+        e.prepare_readback()  # the state's arrays are read back to the host later
         state._e = e
     plan = e.step(e.eval_point(config))
     state._W = state._V = state._Z = None  # written back lazily
@@ -941,6 +960,8 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
     # a CUDA right-hand side keeps the solve on the device: W is returned as
     # this rank's shard (fp32 CUDA tensor), never gathered to n x m
     device_out = torch.is_tensor(Y) and Y.is_cuda
+    if not device_out:
+        eng.prepare_readback()
     try:
         ynorm = eng.y_norm() if device_out else _y_norm(Y)
         trace = ConvergenceTrace()
@@ -979,7 +1000,7 @@ def adasap_solve(oracle, Y, config, identity_precond=False, pool=None, on_iterat
             W_loc = averager.average()
         else:
             W_loc = eng.materialize("W")
-        W = W_loc if device_out else _to_host64(eng.gather_full(W_loc))
+        W = W_loc if device_out else _to_host64(eng.gather_full(W_loc), out=eng.take_readback())
     finally:
         eng.release()
     return SolveResult(W[:, 0] if eng.vector else W, trace, diverged, done, done * b / n)

@@ -65,6 +65,42 @@ def host_pool():
         return _POOL["ex"]
 
 
+# Pre-faulted readback arrays: a fresh float64 host array's first touch costs
+# ~55 ms per 520 MB on one thread (the kernel zeroing its pages), the largest
+# single item of a W readback. An engine bound from host arrays asks for its
+# readback array up front; these threads fault its pages in while the device
+# runs the steps, and the readback then only copies and widens.
+# SAP_PREFAULT_THREADS=0 turns it off.
+_PF_THREADS = int(_os.environ.get("SAP_PREFAULT_THREADS", "4"))
+_PF = {"ex": None}
+
+
+def _touch(a):
+    a[::512] = 0.0  # one store per 4 KB page
+
+
+def prefaulted(shape):
+    """(array, futures): a fresh C-contiguous float64 array of ``shape`` whose
+    pages background threads fault in; wait on the futures before relying on
+    it being resident (its contents are zeros wherever touched, otherwise
+    undefined -- callers overwrite it entirely). None when turned off."""
+    import numpy as np
+    if _PF_THREADS <= 0:
+        return None
+    with _POOL_LOCK:
+        if _PF["ex"] is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _PF["ex"] = ThreadPoolExecutor(max_workers=_PF_THREADS,
+                                           thread_name_prefix="sap-prefault")
+        ex = _PF["ex"]
+    out = np.empty(shape, dtype=np.float64)
+    flat = out.reshape(-1)
+    step = -(-flat.size // _PF_THREADS) if flat.size else 1
+    step = -(-step // 512) * 512  # page-aligned slices
+    futs = [ex.submit(_touch, flat[lo:lo + step]) for lo in range(0, flat.size, step)]
+    return out, futs
+
+
 def _up_staging(nbytes):
     import torch
     buf = _UP["buf"]
