@@ -112,7 +112,10 @@ __device__ __forceinline__ float reduce_splits(const float *pe, int splits, int6
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] += x[u];
   }
-  for (int u = 0; k < splits; ++k, ++u) acc[u] += __ldcg(pe + int64_t(k) * bm);
+  // the < 8 left over, into acc[0..]: static indices keep acc in registers
+#pragma unroll
+  for (int u = 0; u < 7; ++u)
+    if (k + u < splits) acc[u] += __ldcg(pe + int64_t(k + u) * bm);
   return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 }
 
