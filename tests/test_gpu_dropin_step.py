@@ -119,3 +119,33 @@ def test_budgeted_state_raises_contract_error_past_its_budget():
     with pytest.raises(sap.ContractError):
         adasap_step(o, st, Y, cfg, accel)
     st._e.close()
+
+
+def test_prefaulted_readback_is_bitwise_the_plain_one(monkeypatch):
+    """The W readback into the array pre-faulted at bind time
+    (xfer.prefaulted, n*m >= 2^20 here) returns exactly what the plain
+    readback returns, and a second read (no pre-faulted array left) too."""
+    from paper_2505_13723_b200 import xfer
+    rng = np.random.default_rng(5)
+    n, d, m = 20000, 5, 65
+    X = rng.standard_normal((n, d))
+    Y = rng.standard_normal((n, m))
+    o = sap.KernelOracle(sap.KernelSpec("matern32", np.full(d, 2.0), 1.0), X, 1e-2)
+    cfg = sap.RunConfig(lam=1e-2, blocksize=500, nystrom_rank=50, residual_every=0, seed=3)
+    accel = sap.resolve_accel(cfg, n, 500)
+    out = []
+    for threads in (4, 0):
+        monkeypatch.setattr(xfer, "_PF_THREADS", threads)
+        st = SolverState.zeros(n, m, accelerated=True)
+        for _ in range(3):
+            st, _, _ = adasap_step(o, st, Y, cfg, accel)
+        if threads:
+            assert st._e._readback is not None
+        W = st.W
+        assert W.shape == (n, m) and W.dtype == np.float64 and W.flags.c_contiguous
+        st, _, _ = adasap_step(o, st, Y, cfg, accel)
+        out.append((W, st.W))
+        st.iteration = st.iteration  # detach: releases the engine
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert not np.array_equal(out[0][0], out[0][1])
