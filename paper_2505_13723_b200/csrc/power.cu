@@ -83,13 +83,22 @@ __device__ __forceinline__ void block_sum2(double &a, double &c, double *red) {
   }
 }
 
+// rows per CTA (a multiple of 4 with the symmetric sweep: its column blocks
+// start on 16-byte boundaries)
+__host__ __device__ inline int row_block(int b, int C, int sym) {
+  const int per = (b + C - 1) / C;
+  return sym ? (per + 3) & ~3 : per;
+}
+constexpr int kSymCols = 512;  // columns of one sub-range of the symmetric sweep
+
 template <int kCluster>
-__global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const int u_smem) {
+__global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const int u_smem,
+                                                           const int sym) {
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
   const int q = blockIdx.x / kCluster;  // batch element
   const int b = a.b, r = a.r;
-  const int per = (b + kCluster - 1) / kCluster;
+  const int per = row_block(b, kCluster, sym);
   const int lo = min(b, int(crank) * per), hi = min(b, lo + per);
   const int nloc = hi - lo;
   const int b4 = (b + 3) & ~3;
@@ -103,7 +112,12 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   double *red = spart + 2;            // [2*kWarps] block reduction scratch
   double *scratch = red + 2 * kWarps; // [2*kThreads]
   float *wf = reinterpret_cast<float *>(scratch + 2 * kThreads);  // [b4] replicated w (fp32)
-  double *us = reinterpret_cast<double *>(wf + b4);           // [nloc][r] own U rows (opt.)
+  // symmetric sweep only: own rows' direct sums, transposed contributions to
+  // every column (read by the owners over DSMEM), per-warp column partials
+  double *zdir = reinterpret_cast<double *>(wf + b4);         // [per]
+  double *tpart = zdir + (sym ? per : 0);                     // [b4]
+  float *tw = reinterpret_cast<float *>(tpart + (sym ? b4 : 0));  // [kWarps][kSymCols]
+  double *us = reinterpret_cast<double *>(tw + (sym ? kWarps * kSymCols : 0));  // [nloc][r] own U rows (opt.)
 
   const float *K = a.K + int64_t(q) * a.strideK;
   const double *Ug = r ? a.U + int64_t(q) * a.strideU + int64_t(lo) * r : nullptr;
@@ -244,6 +258,117 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
 #else
 #define PP(k) do {} while (0)
 #endif
+  // Symmetric sweep (K_BB is exactly symmetric): the b x b matrix as C x C
+  // blocks of the CTAs' row ranges. CTA c reads, in its own rows, the
+  // diagonal block (c, c), the blocks (c, c+k) for k = 1 .. C/2-1, and half of
+  // (c, c+C/2) (c < C/2: its columns' first half; c >= C/2: its own rows'
+  // second half against all of block c-C/2's columns), and adds each
+  // off-diagonal block's transpose times its own w to the other rows: every
+  // entry of K_BB is read once per step instead of the full matrix, 2.5 of 4
+  // blocks at C = 4 (the sweep is HBM-bound). Direct sums per row in zdir,
+  // transposed ones per column in tpart, combined in a fixed rank order.
+  auto rect = [&](int r0, int r1, int j0, int j1, bool tr) {
+    // empty: no rows, or a column block past b (clamped starts are not
+    // 16-byte aligned); uniform over the CTA
+    if (r1 <= r0 || j1 <= j0) return;
+    const int J1 = min(b4, (j1 + 3) & ~3);
+    for (int s0 = j0; s0 < J1; s0 += kSymCols) {
+      const int s1 = min(J1, s0 + kSymCols);
+      float tacc[kSymCols / 128][4];
+#pragma unroll
+      for (int c = 0; c < kSymCols / 128; ++c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tacc[c][u] = 0.0f;
+      for (int i0 = r0 + warp * kRowsPerPass; i0 < r1; i0 += kWarps * kRowsPerPass) {
+        const float *krow[kRowsPerPass];
+        float wr[kRowsPerPass], acc[kRowsPerPass];
+#pragma unroll
+        for (int rr = 0; rr < kRowsPerPass; ++rr) {
+          const int i = min(i0 + rr, r1 - 1);  // clamped rows: weight 0, sums discarded
+          krow[rr] = K + int64_t(lo + i) * a.ldk;
+          wr[rr] = i0 + rr < r1 ? wf[lo + i0 + rr] : 0.0f;
+          acc[rr] = 0.0f;
+        }
+        float4 kv[kSymCols / 128][kRowsPerPass];
+#pragma unroll
+        for (int c = 0; c < kSymCols / 128; ++c) {
+          const int j = s0 + lane * 4 + 128 * c;
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerPass; ++rr)
+            kv[c][rr] = j < s1 ? __ldg(reinterpret_cast<const float4 *>(krow[rr] + j))
+                               : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int c = 0; c < kSymCols / 128; ++c) {
+          const int j = s0 + lane * 4 + 128 * c;
+          if (j >= s1) break;
+          const float4 w4 = *reinterpret_cast<const float4 *>(wf + j);
+#pragma unroll
+          for (int rr = 0; rr < kRowsPerPass; ++rr) {
+            acc[rr] = fmaf(kv[c][rr].x, w4.x, acc[rr]);
+            acc[rr] = fmaf(kv[c][rr].y, w4.y, acc[rr]);
+            acc[rr] = fmaf(kv[c][rr].z, w4.z, acc[rr]);
+            acc[rr] = fmaf(kv[c][rr].w, w4.w, acc[rr]);
+            if (tr) {
+              tacc[c][0] = fmaf(kv[c][rr].x, wr[rr], tacc[c][0]);
+              tacc[c][1] = fmaf(kv[c][rr].y, wr[rr], tacc[c][1]);
+              tacc[c][2] = fmaf(kv[c][rr].z, wr[rr], tacc[c][2]);
+              tacc[c][3] = fmaf(kv[c][rr].w, wr[rr], tacc[c][3]);
+            }
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kRowsPerPass; ++rr) {
+          const double sd = warp_sum(double(acc[rr]));
+          if (lane == 0 && i0 + rr < r1) zdir[i0 + rr] += sd;
+        }
+      }
+      if (tr) {
+#pragma unroll
+        for (int c = 0; c < kSymCols / 128; ++c)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tw[warp * kSymCols + lane * 4 + 128 * c + u] = tacc[c][u];
+        __syncthreads();
+        for (int jj = tid; jj < s1 - s0; jj += kThreads) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) t += double(tw[w * kSymCols + jj]);
+          tpart[s0 + jj] += t;
+        }
+      }
+      __syncthreads();  // zdir rows / tw reused by the next sub-range or rectangle
+    }
+  };
+  auto blk_lo = [&](int cc) { return min(b, cc * per); };
+  auto blk_hi = [&](int cc) { return min(b, cc * per + per); };
+  auto blk_half = [&](int cc) {
+    const int nn = blk_hi(cc) - blk_lo(cc);
+    return min(nn, ((nn >> 1) + 3) & ~3);
+  };
+  auto sym_sweep = [&]() {
+    for (int i = tid; i < nloc; i += kThreads) zdir[i] = 0.0;
+    for (int j = tid; j < b4; j += kThreads) tpart[j] = 0.0;
+    __syncthreads();
+    const int c = int(crank);
+    rect(0, nloc, lo, hi, false);
+    for (int k = 1; k < kCluster / 2; ++k) {
+      const int cp = (c + k) % kCluster;
+      rect(0, nloc, blk_lo(cp), blk_hi(cp), true);
+    }
+    const int cp = (c + kCluster / 2) % kCluster;
+    if (c < kCluster / 2) rect(0, nloc, blk_lo(cp), blk_lo(cp) + blk_half(cp), true);
+    else rect(blk_half(c), nloc, blk_lo(cp), blk_hi(cp), true);
+    cluster.sync();  // every CTA's tpart complete
+    for (int i = tid; i < nloc; i += kThreads) {
+      double t = 0.0;
+      for (int cc = 0; cc < kCluster; ++cc) t += cluster.map_shared_rank(tpart, cc)[lo + i];
+      zloc[i] = fma(a.lam, zloc[i], zdir[i] + t);
+    }
+    __syncthreads();
+    // peers read this tpart until they pass the next cluster barrier (U^T z's),
+    // which every CTA reaches before zeroing its tpart for the next step
+  };
+
   // The iteration runs on w = P^{-1/2} v rather than on v (the same iterates,
   // Rayleigh quotients and norms, reassociated):
   //   z = (K + lam I) w,  est = v.y = w.z,  |y|^2 = z.P^{-1} z = z.u,
@@ -266,6 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
   PP(0);
   // vloc and zloc hold w on own rows at the top of a step
   for (int it = 0; it < a.iters; ++it) {
+    if (sym) {
+      sym_sweep();
+    } else {
     // z = K w + lam w on own rows: a warp dots kRowsPerPass rows at once, fp32
     // products summed per lane (64 terms for b = 2000), lanes combined in fp64
     for (int i0 = warp * kRowsPerPass; i0 < nloc; i0 += kWarps * kRowsPerPass) {
@@ -323,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
       }
     }
     __syncthreads();
+    }
     PP(3);
     // u = P^{-1} z on own rows, the partials of w.z and z.u
     if (r) ut_times(zloc, true);
@@ -414,10 +543,23 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
   }
   if (C != 4 && C != 8 && C != 16)
     return fail(SAP_ERR_CONTRACT, "power_stepsize: cluster size %d (4, 8 or 16)", C);
-  const int per = (b + C - 1) / C;
+  // the symmetric sweep (half of K_BB's bytes) needs 16-byte rows;
+  // SAP_POWER_SYM=0/1 forces the full / the symmetric sweep
+  const bool vec4 = (ldk & 3) == 0 && (strideK & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(Kbb) & 15) == 0;
+  // (blocks of >= 384 rows: with C = 16 at b = 2000 the many small
+  // rectangles made it 2x slower, 1.07 vs 0.49 ms for 8 iterations; at C = 4
+  // 0.755 vs 0.895 ms for 32)
+  const char *se = getenv("SAP_POWER_SYM");
+  const int sym = (vec4 && ((se && *se) ? atoi(se) != 0 : (b + C - 1) / C >= 384)) ? 1 : 0;
+  const int per = pw::row_block(b, C, sym);
+  const size_t b4 = size_t((b + 3) & ~3);
   const size_t base = sizeof(double) * (2 * size_t(per) + 2 * size_t(r) + 2 + 2 * pw::kWarps +
                                         2 * pw::kThreads) +
-                      sizeof(float) * size_t((b + 3) & ~3);
+                      sizeof(float) * b4 +
+                      (sym ? sizeof(double) * (size_t(per) + b4) +
+                                 sizeof(float) * size_t(pw::kWarps) * pw::kSymCols
+                           : 0);
   const size_t with_u = base + sizeof(double) * size_t(per) * size_t(r);
   constexpr size_t kCap = 200 * 1024;
   if (base > kCap) return fail(SAP_ERR_CONTRACT, "power_stepsize: b=%d exceeds shared memory", b);
@@ -444,9 +586,9 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = C == 4 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<4>, a, u_smem)
-                        : C == 8 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<8>, a, u_smem)
-                                 : cudaLaunchKernelEx(&cfg, pw::power_kernel<16>, a, u_smem);
+  const cudaError_t e = C == 4 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<4>, a, u_smem, sym)
+                        : C == 8 ? cudaLaunchKernelEx(&cfg, pw::power_kernel<8>, a, u_smem, sym)
+                                 : cudaLaunchKernelEx(&cfg, pw::power_kernel<16>, a, u_smem, sym);
   if (e != cudaSuccess) return fail(SAP_ERR_DEVICE, "power_kernel: %s", cudaGetErrorString(e));
   return check_launch("power_kernel");
 }
