@@ -551,17 +551,22 @@ extern "C" int sap_power_stepsize(const float *Kbb, int64_t ldk, int64_t strideK
   // rectangles made it 2x slower, 1.07 vs 0.49 ms for 8 iterations; at C = 4
   // 0.755 vs 0.895 ms for 32)
   const char *se = getenv("SAP_POWER_SYM");
-  const int sym = (vec4 && ((se && *se) ? atoi(se) != 0 : (b + C - 1) / C >= 384)) ? 1 : 0;
-  const int per = pw::row_block(b, C, sym);
   const size_t b4 = size_t((b + 3) & ~3);
-  const size_t base = sizeof(double) * (2 * size_t(per) + 2 * size_t(r) + 2 + 2 * pw::kWarps +
-                                        2 * pw::kThreads) +
-                      sizeof(float) * b4 +
-                      (sym ? sizeof(double) * (size_t(per) + b4) +
-                                 sizeof(float) * size_t(pw::kWarps) * pw::kSymCols
-                           : 0);
-  const size_t with_u = base + sizeof(double) * size_t(per) * size_t(r);
+  auto smem_base = [&](int sy) {
+    const size_t pr = size_t(pw::row_block(b, C, sy));
+    return sizeof(double) * (2 * pr + 2 * size_t(r) + 2 + 2 * pw::kWarps + 2 * pw::kThreads) +
+           sizeof(float) * b4 +
+           (sy ? sizeof(double) * (pr + b4) + sizeof(float) * size_t(pw::kWarps) * pw::kSymCols
+               : 0);
+  };
   constexpr size_t kCap = 200 * 1024;
+  // the symmetric sweep's extra shared memory (~b x 8 bytes more) must fit
+  // too: at b = 10 000 (config 5) it does not, and the full sweep runs
+  const int sym = (vec4 && ((se && *se) ? atoi(se) != 0 : (b + C - 1) / C >= 384) &&
+                   smem_base(1) <= kCap) ? 1 : 0;
+  const int per = pw::row_block(b, C, sym);
+  const size_t base = smem_base(sym);
+  const size_t with_u = base + sizeof(double) * size_t(per) * size_t(r);
   if (base > kCap) return fail(SAP_ERR_CONTRACT, "power_stepsize: b=%d exceeds shared memory", b);
   const int u_smem = with_u <= kCap ? 1 : 0;
   const size_t smem = u_smem ? with_u : base;

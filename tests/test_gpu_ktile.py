@@ -48,14 +48,16 @@ def test_ktile_batch_bitwise(family, b, d):
 @pytest.mark.parametrize("sym", [None, "1"])
 @pytest.mark.parametrize("cluster", ["4", "8", "16", None])
 @pytest.mark.parametrize("count,b,r", [(32, 2000, 100), (5, 1000, 100), (3, 130, 7), (2, 64, 0),
-                                       (2, 333, 5), (2, 332, 5), (3, 124, 6), (2, 20, 3)])
+                                       (2, 333, 5), (2, 332, 5), (3, 124, 6), (2, 20, 3),
+                                       (2, 10000, 20)])
 def test_power_stepsize_cluster_sizes(sym, cluster, count, b, r, monkeypatch):
     """sap_power_stepsize (csrc/power.cu; randnla.py:165-196) for every cluster
     size the launcher picks (None: its own choice, one wave when it can), with
     the launcher's choice of sweep and with the symmetric sweep forced (empty
-    and partial column blocks at small b; rows not 16-byte aligned fall back
-    to the full sweep), against the same preconditioned power iteration in
-    torch fp64."""
+    and partial column blocks at small b; rows not 16-byte aligned, or a
+    symmetric sweep too large for shared memory (b = 10 000 at C = 4), fall
+    back to the full sweep), against the same preconditioned power iteration
+    in torch fp64."""
     if cluster is None:
         monkeypatch.delenv("SAP_POWER_CLUSTER", raising=False)
     else:
