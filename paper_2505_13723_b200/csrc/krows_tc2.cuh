@@ -183,6 +183,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc::cluster_sync();  // barriers of both CTAs initialised before any remote signal
   tc::fence_after();
+  // launched with programmatic stream serialization: the set-up above (barrier
+  // init, TMEM allocation, descriptor prefetch, arming the NEXT launch's
+  // counter slot) may overlap the previous kernel's tail; everything below
+  // reads or writes what earlier kernels produce or consume (features, the
+  // operand, the partials), so it waits for them (a no-op when not launched
+  // as a dependent)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const int units = p.row_tiles * p.splits;  // row_tiles counts 256-row pair tiles here
   // Units (256-row tile x column split) are handed out dynamically: the
@@ -589,7 +596,21 @@ bool launch_tc2_shape(const CUtensorMap &a, const CUtensorMap &c, const CUtensor
     constexpr uint32_t smem = Geometry2<NZ, KA, H>::smem;
     cudaFuncSetAttribute(krows_tc2_kernel<FAM, NZ, KA, H>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    krows_tc2_kernel<FAM, NZ, KA, H><<<grid, kThreads, smem, st>>>(a, c, zh, zl, p);
+    // programmatic dependent launch (SAP_TC_PDL=0: plain stream order): the
+    // grid is scheduled while the previous kernel (Phase IV's last stage)
+    // drains, hiding the launch gap
+    static const bool pdl = !(getenv("SAP_TC_PDL") && atoi(getenv("SAP_TC_PDL")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, krows_tc2_kernel<FAM, NZ, KA, H>, a, c, zh, zl, p);
     return true;
   }
 }
