@@ -176,3 +176,21 @@ def test_batched_device_factor_matches_host_factor():
         np.testing.assert_allclose(E[i].numpy(), 1.0 / np.sqrt(Sh + rho_h) - 1.0 / np.sqrt(rho_h),
                                    rtol=1e-8, atol=1e-12)
     assert not flags.any()
+
+
+def test_prefaulted_readback_array(monkeypatch):
+    """xfer.prefaulted: a C-contiguous float64 array of the asked shape whose
+    pages the background threads have touched once the futures are done
+    (every 512th element zeroed), page-aligned slices, and off with 0 threads."""
+    from paper_2505_13723_b200 import xfer
+    monkeypatch.setattr(xfer, "_PF_THREADS", 3)
+    out, futs = xfer.prefaulted((1001, 7))
+    for f in futs:
+        f.result()
+    assert out.shape == (1001, 7) and out.dtype == np.float64 and out.flags.c_contiguous
+    assert len(futs) == 3
+    assert np.all(out.reshape(-1)[::512] == 0.0)
+    out0, futs0 = xfer.prefaulted((0, 5))
+    assert out0.shape == (0, 5) and not futs0
+    monkeypatch.setattr(xfer, "_PF_THREADS", 0)
+    assert xfer.prefaulted((10, 10)) is None
