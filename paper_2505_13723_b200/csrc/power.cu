@@ -365,8 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1) power_kernel(const Args a, const 
       zloc[i] = fma(a.lam, zloc[i], zdir[i] + t);
     }
     __syncthreads();
-    // peers read this tpart until they pass the next cluster barrier (U^T z's),
-    // which every CTA reaches before zeroing its tpart for the next step
+    // peers read this tpart before they reach the step's next cluster barrier
+    // (U^T z's, or the scalars' when r = 0), which every CTA passes before it
+    // zeroes its tpart for the next step
   };
 
   // The iteration runs on w = P^{-1/2} v rather than on v (the same iterates,
