@@ -177,6 +177,7 @@ class TcPoints:
         # every magnitude stays inside fp16's range (|z|^2 < 2^14 leaves room
         # for the -2 z column form); SAP_TC_F16=0 keeps fp32
         # (d >= 10 needs 64 features: fp16 too, 128-byte rows, since round 2)
+        xfer.mark("tc points: features")
         self.half = False
         if os.environ.get("SAP_TC_F16", "1") == "1":
             zmax2 = _CFAM[spec.family] * float(((Xd * inv) ** 2).sum(1).max())
@@ -184,6 +185,7 @@ class TcPoints:
         self.ka_code = ((nat.SAP_TC_KA_F16 if self.ka == 32 else nat.SAP_TC_KA_F16X64)
                         if self.half else self.ka)
         self.dtype = torch.float16 if self.half else torch.float32
+        xfer.mark("tc points: range check")
         if self.half:
             self.CA = self.CA.half()
 

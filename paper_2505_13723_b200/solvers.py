@@ -482,6 +482,7 @@ class AdasapEngine:
         self.ld = max(4, (nl + 3) // 4 * 4)
         f32 = torch.float32
         b, m = self.b, self.m
+        xfer.mark("bind: start")
         self.use_tc = oracle.use_tc(m) and b >= 16 and nl > 0 and not self.dense
         self.tcp = oracle.tc_points(self.shard.lo, self.shard.hi) if self.use_tc else None
         # the lookahead first: its first plans (which need neither Y nor the
