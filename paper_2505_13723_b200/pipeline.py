@@ -105,9 +105,12 @@ class _Slot:
         self.v0 = torch.empty((L, b), dtype=f64, device=dev)
         # K_BB in fp32: the values the tile kernel computes (fp32 arithmetic),
         # streamed once per power step by sap_power_stepsize
-        # zeroed: the power kernel reads rows in 16-byte chunks through the pad
-        # columns (times a zero w); never-written pad bits must not be NaN
-        self.Kbb = torch.zeros((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
+        # zeroed when rows are padded: the power kernel reads rows in 16-byte
+        # chunks through the pad columns (times a zero w), and never-written
+        # pad bits must not be NaN; with b % 4 == 0 there is no pad and the
+        # tile kernel writes every entry a plan uses (no 512 MB memset per slot)
+        alloc = torch.empty if b % 4 == 0 else torch.zeros
+        self.Kbb = alloc((L, b, (b + 3) // 4 * 4), dtype=torch.float32, device=dev)
         self.eta = torch.empty(L, dtype=f64, device=dev)
         self.eta_rho = torch.empty(L, dtype=f64, device=dev)  # eta / rho (Phase IV's 1/rho folded)
         self.bad = torch.zeros(L, dtype=torch.int32, device=dev)
