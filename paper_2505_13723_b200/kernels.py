@@ -408,11 +408,14 @@ class KernelOracle:
             self._Xd = Xn.to(device=self.device, dtype=torch.float64).contiguous()
         else:
             self._Xd = xfer.upload(Xn, torch.float64, self.device)
+        xfer.mark("oracle: X upload")
         # the reference's finiteness check (kernels.py:100-112), on the device
         # copy: np.isfinite over a 10^6 x 9 host array alone took ~10 ms
         if not bool(torch.isfinite(self._Xd).all()):
             raise ValidationError("non-finite training inputs")
+        xfer.mark("oracle: finite check")
         self.points = DevicePoints(spec, self._Xd, self.device)
+        xfer.mark("oracle: points")
         self._ws = None
         self._tc = None
         self.backend = "auto"  # "tc" (tcgen05), "ffma", or "auto" (tc when the shape fits)

@@ -38,9 +38,9 @@ for rep in range(int(os.environ.get("REPS", "8"))):
                   f"enqueue {1e3 * tm['gpu_wait']:.1f}, factor {1e3 * tm['factor']:.1f})")
     from paper_2505_13723_b200 import xfer
     if xfer.TRACE is not None:  # SAP_TRACE=1
-        for tt, th, tag in xfer.TRACE:
-            if tt >= T[1]:
-                print(f"   {1e3 * (tt - T[1]):8.2f} ms  {th:22s} {tag}")
+        for tt, th, tag in xfer.TRACE:  # from the start of the rep (oracle included)
+            if tt >= T[0]:
+                print(f"   {1e3 * (tt - T[0]):8.2f} ms  {th:22s} {tag}")
         xfer.TRACE.clear()
     W = st.W; torch.cuda.synchronize(); T.append(time.perf_counter())
     st.iteration = st.iteration; T.append(time.perf_counter())
